@@ -1,0 +1,378 @@
+// capi.cu -- the C-ABI boundary (include/convgemm_b200.h): geometry validation with
+// the reference's error semantics, operator/precision selection, device workspace
+// accounting (the ScratchTracker equivalent) and kernel dispatch.
+//
+// Reference interfaces replaced (all under /root/reference/proj/include/convgemm/):
+//   conv_gemm            conv.hpp:78-91     -> cgb_conv(CGB_ALGO_FUSED, ...)
+//   conv_im2col_gemm     conv.hpp:60-74     -> cgb_conv(CGB_ALGO_EXPLICIT, ...)
+//   im2col               im2col.hpp:77-120  -> cgb_im2col
+//   output_dims/gemm_dims conv_params.hpp:27-43
+//   ScratchTracker       scratch.hpp:14-28, src/scratch.cpp:12-52
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/convgemm_b200.h"
+#include "internal.h"
+
+namespace cgb {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static thread_local std::string g_last_error;
+static thread_local int g_last_path = 0;
+
+static cgb_status fail(cgb_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+static cgb_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(CGB_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ geometry (conv_params.hpp:27-43)
+static cgb_status make_geom(const cgb_conv_params* cp, ConvGeom* g) {
+  if (!cp) return fail(CGB_INVALID_ARGUMENT, "null ConvParams");
+  if (cp->k_n < 1 || cp->k_h < 1 || cp->k_w < 1 || cp->c_i < 1 || cp->h_i < 1 || cp->w_i < 1 || cp->b < 1 ||
+      cp->s < 1 || cp->p < 0)
+    return fail(CGB_INVALID_GEOMETRY, "conv extents must be positive (padding non-negative)");
+  const int64_t dh = cp->h_i - cp->k_h + 2 * cp->p;
+  const int64_t dw = cp->w_i - cp->k_w + 2 * cp->p;
+  if (dh < 0 || dw < 0) return fail(CGB_INVALID_GEOMETRY, "filter exceeds padded input");
+  g->k_n = cp->k_n; g->k_h = cp->k_h; g->k_w = cp->k_w; g->c_i = cp->c_i;
+  g->h_i = cp->h_i; g->w_i = cp->w_i; g->b = cp->b; g->s = cp->s; g->p = cp->p;
+  g->h_o = dh / cp->s + 1;
+  g->w_o = dw / cp->s + 1;
+  g->m = cp->k_n;
+  g->n = g->h_o * g->w_o * cp->b;
+  g->k = cp->k_h * cp->k_w * cp->c_i;
+  return CGB_OK;
+}
+
+// Index-width limits of the device kernels (32-bit per-image / per-row offsets).
+static cgb_status check_device_limits(const ConvGeom& g) {
+  const int64_t lim = (int64_t(1) << 31) - 1;
+  if (g.c_i * g.h_i * g.w_i > lim || g.k > lim || g.h_o * g.w_o > lim || g.k_n > lim)
+    return fail(CGB_UNSUPPORTED, "per-image extents exceed the 32-bit device indexing range");
+  return CGB_OK;
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+cudaError_t make_filter_tmap(CUtensorMap* tm, const float* f, int64_t k_n, int64_t K, int64_t ldf) {
+  auto enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)k_n, (cuuint64_t)K};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldf * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(f), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ workspace (ScratchTracker)
+struct Scratch {
+  std::mutex mu;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+  std::atomic<uint64_t> current{0}, peak{0}, limit{0};
+};
+static Scratch g_scratch;
+
+static cgb_status scratch_get(size_t need, void** out) {
+  std::lock_guard<std::mutex> lk(g_scratch.mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_scratch.ptr && g_scratch.bytes >= need && g_scratch.device == dev) {
+    *out = g_scratch.ptr;
+    return CGB_OK;
+  }
+  const uint64_t lim = g_scratch.limit.load();
+  const uint64_t keep = (g_scratch.device == dev) ? 0 : 0;
+  (void)keep;
+  if (lim != 0 && need > lim)
+    return fail(CGB_ALLOCATION_FAILURE, "workspace limit exceeded: " + std::to_string(need) +
+                                            " bytes requested, limit " + std::to_string(lim));
+  if (g_scratch.ptr) {
+    cudaFree(g_scratch.ptr);  // synchronises: no kernel still reads the old buffer
+    g_scratch.current.store(0);
+    g_scratch.ptr = nullptr;
+    g_scratch.bytes = 0;
+  }
+  void* p = nullptr;
+  const size_t alloc = std::max<size_t>(need, size_t(1) << 20);
+  if (cudaMalloc(&p, alloc) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CGB_ALLOCATION_FAILURE, "cannot allocate " + std::to_string(alloc) + " bytes of device workspace");
+  }
+  g_scratch.ptr = p;
+  g_scratch.bytes = alloc;
+  g_scratch.device = dev;
+  g_scratch.current.store(alloc);
+  uint64_t seen = g_scratch.peak.load();
+  while (seen < alloc && !g_scratch.peak.compare_exchange_weak(seen, alloc)) {
+  }
+  *out = p;
+  return CGB_OK;
+}
+
+static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Workspace plan for one call: filter copies (hi[, lo]) then B-hat.
+struct Plan {
+  int algo, prec;
+  bool direct_filters;  // TF32 mode reading F itself through TMA (no filter workspace)
+  int64_t ldf, ldb;
+  int64_t f_bytes, b_bytes;
+};
+
+static bool tf32_family(int prec) { return prec == CGB_PREC_TF32 || prec == CGB_PREC_3XTF32; }
+
+static int resolve_precision(int prec, const ConvGeom& g) {
+  if (prec != CGB_PREC_AUTO) return prec;
+  // fp32-accurate choice: FFMA where the contraction is too short to feed the tensor
+  // cores (K < 32, e.g. VGG conv1 with K = 27), 3xTF32 otherwise.
+  return g.k < 32 ? CGB_PREC_FFMA : CGB_PREC_3XTF32;
+}
+
+static Plan make_plan(int algo, int prec, const ConvGeom& g, const float* F) {
+  Plan pl{};
+  pl.algo = algo;
+  pl.prec = prec;
+  pl.ldf = align_up(g.k_n, 4);
+  pl.direct_filters = prec == CGB_PREC_TF32 && g.k_n % 4 == 0 &&
+                      (F == nullptr || reinterpret_cast<uintptr_t>(F) % 16 == 0);
+  if (tf32_family(prec) && !pl.direct_filters)
+    pl.f_bytes = align_up(pl.ldf * g.k * 4, 256) * (prec == CGB_PREC_3XTF32 ? 2 : 1);
+  pl.ldb = align_up(g.k, 4);
+  if (algo == CGB_ALGO_EXPLICIT) pl.b_bytes = align_up(pl.ldb * g.n * 4, 256);
+  return pl;
+}
+
+}  // namespace cgb
+
+using namespace cgb;
+
+extern "C" {
+
+cgb_status cgb_output_dims(const cgb_conv_params* cp, int64_t* h_o, int64_t* w_o) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (h_o) *h_o = g.h_o;
+  if (w_o) *w_o = g.w_o;
+  return CGB_OK;
+}
+
+cgb_status cgb_gemm_dims(const cgb_conv_params* cp, int64_t* m, int64_t* n, int64_t* k) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (m) *m = g.m;
+  if (n) *n = g.n;
+  if (k) *k = g.k;
+  return CGB_OK;
+}
+
+int64_t cgb_im2col_workspace_bytes(const cgb_conv_params* cp) {
+  ConvGeom g;
+  if (make_geom(cp, &g)) return -1;
+  return g.k * g.n * (int64_t)sizeof(float);
+}
+
+cgb_status cgb_validate_blocking(const cgb_blocking_params* bp) {
+  if (!bp) return CGB_OK;  // BlockingParams{} defaults are valid
+  if (bp->mc < 1 || bp->nc < 1 || bp->kc < 1 || bp->mr < 1 || bp->nr < 1)
+    return fail(CGB_INVALID_ARGUMENT, "blocking parameters must be positive");
+  if (bp->mr > bp->mc || bp->nr > bp->nc)
+    return fail(CGB_INVALID_ARGUMENT, "micro-tile must fit the cache block (mr<=mc, nr<=nc)");
+  if (bp->mr * bp->nr > 4096) return fail(CGB_INVALID_ARGUMENT, "micro-tile mr*nr exceeds the supported maximum");
+  return CGB_OK;
+}
+
+int64_t cgb_conv_workspace_bytes(int algo, int precision, const cgb_conv_params* cp) {
+  ConvGeom g;
+  if (make_geom(cp, &g)) return -1;
+  const Plan pl = make_plan(algo, resolve_precision(precision, g), g, nullptr);
+  return pl.f_bytes + pl.b_bytes;
+}
+
+cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, const cgb_conv_params* cp, float* O,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (algo != CGB_ALGO_EXPLICIT && algo != CGB_ALGO_FUSED) return fail(CGB_INVALID_ARGUMENT, "unknown algo");
+  if (precision < CGB_PREC_AUTO || precision > CGB_PREC_FFMA)
+    return fail(CGB_INVALID_ARGUMENT, "unknown precision");
+  if (!F || !I || !O) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  if ((st = check_device_limits(g))) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int prec = resolve_precision(precision, g);
+  const Plan pl = make_plan(algo, prec, g, F);
+  const size_t need = (size_t)(pl.f_bytes + pl.b_bytes);
+  uint8_t* ws = nullptr;
+  if (need > 0) {
+    if (workspace) {
+      if (workspace_bytes < need)
+        return fail(CGB_ALLOCATION_FAILURE, "caller workspace too small: need " + std::to_string(need) + " bytes");
+      ws = static_cast<uint8_t*>(workspace);
+    } else {
+      void* p = nullptr;
+      if ((st = scratch_get(need, &p))) return st;
+      ws = static_cast<uint8_t*>(p);
+    }
+  }
+  cudaError_t e;
+  // Filters for the tensor-core paths.
+  const float* f_hi = F;
+  const float* f_lo = nullptr;
+  int64_t ldf = g.k_n;
+  if (tf32_family(prec)) {
+    if (pl.direct_filters) {
+      f_hi = F;
+      ldf = g.k_n;
+    } else {
+      float* hi = reinterpret_cast<float*>(ws);
+      float* lo = prec == CGB_PREC_3XTF32 ? reinterpret_cast<float*>(ws + pl.f_bytes / 2) : nullptr;
+      if ((e = launch_filter_prep(F, hi, lo, pl.ldf, g, s)) != cudaSuccess) return cuda_fail(e, "filter_prep");
+      f_hi = hi;
+      f_lo = lo;
+      ldf = pl.ldf;
+    }
+  }
+  const float* Bhat = nullptr;
+  if (algo == CGB_ALGO_EXPLICIT) {
+    float* B = reinterpret_cast<float*>(ws + pl.f_bytes);
+    if ((e = launch_im2col(I, B, pl.ldb, g, s)) != cudaSuccess) return cuda_fail(e, "im2col");
+    Bhat = B;
+  }
+  if (prec == CGB_PREC_FFMA) {
+    e = launch_ffma_conv(F, I, Bhat, pl.ldb, O, g, s);
+    g_last_path = Bhat ? 4 : 3;
+  } else {
+    const bool split = prec == CGB_PREC_3XTF32;
+    if (!Bhat && shifted_supported(g)) {
+      e = launch_tc_conv_shifted(f_hi, f_lo, ldf, I, O, g, split, s);
+      g_last_path = 5;
+    } else {
+      e = launch_tc_conv(f_hi, f_lo, ldf, I, Bhat, pl.ldb, O, g, split, s);
+      g_last_path = Bhat ? 2 : 1;
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "conv kernel launch");
+  return CGB_OK;
+}
+
+cgb_status cgb_conv_gemm(const float* F, const float* I, const cgb_conv_params* cp, const cgb_blocking_params* bp,
+                         int threads, float* O, int precision, void* stream) {
+  (void)threads;
+  cgb_status st = cgb_validate_blocking(bp);
+  if (st) return st;
+  return cgb_conv(CGB_ALGO_FUSED, precision, F, I, cp, O, nullptr, 0, stream);
+}
+
+cgb_status cgb_conv_im2col_gemm(const float* F, const float* I, const cgb_conv_params* cp,
+                                const cgb_blocking_params* bp, int threads, float* O, int precision, void* stream) {
+  (void)threads;
+  cgb_status st = cgb_validate_blocking(bp);
+  if (st) return st;
+  return cgb_conv(CGB_ALGO_EXPLICIT, precision, F, I, cp, O, nullptr, 0, stream);
+}
+
+cgb_status cgb_im2col(const float* I, const cgb_conv_params* cp, float* B, int64_t ldb, void* stream) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (!I || !B) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  if (ldb < g.k) return fail(CGB_DIMENSION_MISMATCH, "leading dimension smaller than k");
+  if ((st = check_device_limits(g))) return st;
+  cudaError_t e = launch_im2col(I, B, ldb, g, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "im2col");
+  return CGB_OK;
+}
+
+// Host-memory entry point with the reference's synchronous semantics.
+cgb_status cgb_conv_host(int algo, int precision, const float* F_host, const float* I_host,
+                         const cgb_conv_params* cp, float* O_host, void* stream) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (!F_host || !I_host || !O_host) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t fb = (size_t)(g.k_n * g.k) * 4, ib = (size_t)(g.c_i * g.h_i * g.w_i * g.b) * 4,
+               ob = (size_t)(g.k_n * g.n) * 4;
+  // Device staging buffers for the host path, cached across calls (not workspace).
+  static std::mutex mu;
+  static void* buf = nullptr;
+  static size_t cap = 0;
+  static int dev_of_buf = -1;
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t need = (size_t)align_up((int64_t)fb, 256) + (size_t)align_up((int64_t)ib, 256) + ob;
+  if (!buf || cap < need || dev_of_buf != dev) {
+    if (buf) cudaFree(buf);
+    buf = nullptr;
+    if (cudaMalloc(&buf, need) != cudaSuccess) {
+      cudaGetLastError();
+      cap = 0;
+      return fail(CGB_ALLOCATION_FAILURE, "cannot allocate device staging for the host path");
+    }
+    cap = need;
+    dev_of_buf = dev;
+  }
+  uint8_t* b = static_cast<uint8_t*>(buf);
+  float* dF = reinterpret_cast<float*>(b);
+  float* dI = reinterpret_cast<float*>(b + align_up((int64_t)fb, 256));
+  float* dO = reinterpret_cast<float*>(b + align_up((int64_t)fb, 256) + align_up((int64_t)ib, 256));
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(dF, F_host, fb, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D F");
+  if ((e = cudaMemcpyAsync(dI, I_host, ib, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D I");
+  st = cgb_conv(algo, precision, dF, dI, cp, dO, nullptr, 0, stream);
+  if (st) return st;
+  if ((e = cudaMemcpyAsync(O_host, dO, ob, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return cuda_fail(e, "D2H O");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "sync");
+  return CGB_OK;
+}
+
+uint64_t cgb_scratch_current_bytes(void) { return g_scratch.current.load(); }
+uint64_t cgb_scratch_peak_bytes(void) { return g_scratch.peak.load(); }
+void cgb_scratch_reset_peak(void) { g_scratch.peak.store(g_scratch.current.load()); }
+void cgb_scratch_set_limit(uint64_t bytes) { g_scratch.limit.store(bytes); }
+void cgb_scratch_release(void) {
+  std::lock_guard<std::mutex> lk(g_scratch.mu);
+  if (g_scratch.ptr) cudaFree(g_scratch.ptr);
+  g_scratch.ptr = nullptr;
+  g_scratch.bytes = 0;
+  g_scratch.current.store(0);
+}
+
+const char* cgb_last_error(void) { return g_last_error.c_str(); }
+const char* cgb_version(void) { return "convgemm-b200 0.1 (sm_100a)"; }
+uint64_t cgb_kernel_launch_count(void) { return g_launches.load(); }
+int cgb_last_path(void) { return g_last_path; }
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// internal.h -- host-side interfaces between the C-ABI layer (capi.cu) and the
+// kernel translation units. Not installed; no torch types.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace cgb {
+
+// Launch accounting (cgb_kernel_launch_count): every kernel launch site bumps it.
+void count_launch(uint64_t n = 1);
+
+// K1: explicit lowered matrix B (k x n, column-major, ld = ldb >= k), bit-exact
+// with im2col<float> (im2col.hpp:77-120); rows k..ldb-1 zero-filled.
+cudaError_t launch_im2col(const float* I, float* B, int64_t ldb, const ConvGeom& g, cudaStream_t st);
+
+// K4: fp32 FFMA convolution on CUDA cores. explicit_src != nullptr selects the
+// explicit path (A operand read from B with leading dimension ldb).
+cudaError_t launch_ffma_conv(const float* F, const float* I, const float* explicit_src, int64_t ldb, float* O,
+                             const ConvGeom& g, cudaStream_t st);
+
+// K5: filter preparation. Writes F (k_n x K, ld = k_n) into hi (and lo when
+// lo != nullptr) with leading dimension ldf >= k_n, zero padding n >= k_n.
+// hi = tf32_rna(f), lo = tf32_rna(f - hi)  (3xTF32 split); with lo == nullptr hi = f.
+cudaError_t launch_filter_prep(const float* F, float* hi, float* lo, int64_t ldf, const ConvGeom& g,
+                               cudaStream_t st);
+
+// K2/K3: tcgen05 kind::tf32 implicit GEMM. Filters are read by TMA from
+// (f_hi, f_lo) with leading dimension ldf (ldf*4 % 16 == 0). explicit_src selects
+// the explicit path (A rows from B with leading dimension ldb, ldb % 4 == 0).
+cudaError_t launch_tc_conv(const float* f_hi, const float* f_lo, int64_t ldf, const float* I,
+                           const float* explicit_src, int64_t ldb, float* O, const ConvGeom& g, bool split,
+                           cudaStream_t st);
+
+// 2-D TMA descriptor over a filter matrix (k_n x K, leading dimension ldf floats):
+// box 32 filters x 32 rows, 128-byte swizzle (the MN-major UMMA B layout).
+cudaError_t make_filter_tmap(CUtensorMap* tm, const float* f, int64_t k_n, int64_t K, int64_t ldf);
+
+// V2: stride/phase "shifted window" tcgen05 kernel; returns cudaErrorNotSupported
+// when the geometry is outside its domain (caller falls back to launch_tc_conv).
+bool shifted_supported(const ConvGeom& g);
+cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t ldf, const float* I, float* O,
+                                   const ConvGeom& g, bool split, cudaStream_t st);
+
+}  // namespace cgb

@@ -1,0 +1,216 @@
+"""GPU parity: the B200 operator through the C-ABI against the reference's outputs.
+
+Bars (BASELINE.json north_star), per-output normalised by ||F[i_k]||*||B[:,col]||:
+  3xTF32 and FFMA <= 1e-5, TF32 <= 5e-3; im2col (pure data movement) bit-exact.
+Oracles: committed golden fixtures produced by the reference itself
+(tests/golden/make_golden.py) and the plain-C restatement (oracle/, pinned
+bitwise to the reference by tests/test_oracle.py) for larger shapes.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import paper_2005_06410_b200 as cg  # noqa: E402
+from conftest import golden_cases  # noqa: E402
+from oracle.oracle import Restatement, per_output_error  # noqa: E402
+
+TOL = {"3xtf32": 1e-5, "ffma": 1e-5, "tf32": 5e-3, "auto": 1e-5}
+PRECS = ("3xtf32", "tf32", "ffma")
+ALGOS = ("fused", "explicit")
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Restatement()
+
+
+def to_dev(a):
+    """numpy Fortran array -> leftmost-fastest CUDA tensor with identical layout."""
+    a = np.asfortranarray(a, dtype=np.float32)
+    t = torch.from_numpy(a.reshape(-1, order="F").copy()).cuda()
+    d = a.shape
+    return t.view(d[3], d[2], d[1], d[0]).permute(3, 2, 1, 0)
+
+
+def to_host(t):
+    d = t.shape
+    flat = t.permute(3, 2, 1, 0).contiguous().view(-1).cpu().numpy()
+    return flat.reshape(d, order="F")
+
+
+def rand_inputs(cp, seed, stem=False):
+    rng = np.random.default_rng(seed)
+    fs = (cp["k_n"], cp["k_h"], cp["k_w"], cp["c_i"])
+    is_ = (cp["h_i"], cp["w_i"], cp["c_i"], cp["b"])
+    if stem:
+        F = rng.normal(0.0, 0.05, fs).astype(np.float32)
+        I = rng.uniform(0.0, 1.0, is_).astype(np.float32)
+    else:
+        F = rng.uniform(-1, 1, fs).astype(np.float32)
+        I = rng.uniform(-1, 1, is_).astype(np.float32)
+    return np.asfortranarray(F), np.asfortranarray(I)
+
+
+# ---------------------------------------------------------------- im2col (K1): bit-exact
+def test_im2col_bitexact_golden(golden):
+    for i, cp, g in golden_cases(golden, "rand"):
+        B = cg.im2col(to_dev(g[f"rand{i}_I"]), cp)
+        assert np.array_equal(B.cpu().numpy(), g[f"rand{i}_B"]), (i, cp)
+
+
+def test_im2col_padded_ld_and_medium(golden, orc):
+    for i, cp, g in golden_cases(golden, "med"):
+        I = g[f"med{i}_I"]
+        k = cp["k_h"] * cp["k_w"] * cp["c_i"]
+        for ldb in (k, (k + 3) // 4 * 4, k + 5):
+            B = cg.im2col(to_dev(I), cp, ldb=ldb)
+            assert np.array_equal(B.cpu().numpy(), orc.im2col(np.asfortranarray(I), cp)), (i, ldb)
+
+
+# ---------------------------------------------------------------- conv vs golden reference outputs
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("prec", PRECS)
+def test_conv_golden_random(golden, orc, algo, prec):
+    worst = 0.0
+    for i, cp, g in golden_cases(golden, "rand"):
+        F, I = np.asfortranarray(g[f"rand{i}_F"]), np.asfortranarray(g[f"rand{i}_I"])
+        O = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo=algo, precision=prec))
+        err = per_output_error(O, g[f"rand{i}_O"], orc.output_scale(F, I, cp))
+        worst = max(worst, err)
+        assert err <= TOL[prec], (i, cp, err)
+    print(f"{algo}/{prec}: worst per-output error {worst:.3e} over 64 reference configs")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("prec", PRECS)
+def test_conv_golden_medium(golden, orc, algo, prec):
+    for i, cp, g in golden_cases(golden, "med"):
+        F, I = np.asfortranarray(g[f"med{i}_F"]), np.asfortranarray(g[f"med{i}_I"])
+        O = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo=algo, precision=prec))
+        err = per_output_error(O, g[f"med{i}_O"], orc.output_scale(F, I, cp))
+        assert err <= TOL[prec], (i, cp, err)
+
+
+# ---------------------------------------------------------------- BASELINE geometries (reduced batch)
+BASELINE_LAYERS = {
+    "c1_56_64_b8": (dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=56, w_i=56, b=8, s=1, p=1), False),
+    "r50_28_128": (dict(k_n=128, k_h=3, k_w=3, c_i=128, h_i=28, w_i=28, b=2, s=1, p=1), False),
+    "r50_14_256": (dict(k_n=256, k_h=3, k_w=3, c_i=256, h_i=14, w_i=14, b=2, s=1, p=1), False),
+    "r50_7_512": (dict(k_n=512, k_h=3, k_w=3, c_i=512, h_i=7, w_i=7, b=2, s=1, p=1), False),
+    "r50_s2_56": (dict(k_n=128, k_h=3, k_w=3, c_i=128, h_i=56, w_i=56, b=1, s=2, p=1), False),
+    "r50_s2_28": (dict(k_n=256, k_h=3, k_w=3, c_i=256, h_i=28, w_i=28, b=1, s=2, p=1), False),
+    "r50_s2_14": (dict(k_n=512, k_h=3, k_w=3, c_i=512, h_i=14, w_i=14, b=2, s=2, p=1), False),
+    "pw_56_64_256": (dict(k_n=256, k_h=1, k_w=1, c_i=64, h_i=56, w_i=56, b=2, s=1, p=0), False),
+    "pw_7_512_2048": (dict(k_n=2048, k_h=1, k_w=1, c_i=512, h_i=7, w_i=7, b=2, s=1, p=0), False),
+    "stem_224": (dict(k_n=64, k_h=7, k_w=7, c_i=3, h_i=224, w_i=224, b=1, s=2, p=3), True),
+    "vgg_conv1": (dict(k_n=64, k_h=3, k_w=3, c_i=3, h_i=224, w_i=224, b=1, s=1, p=1), False),
+}
+
+
+@pytest.mark.parametrize("name", sorted(BASELINE_LAYERS))
+@pytest.mark.parametrize("prec", ("3xtf32", "tf32", "auto"))
+def test_conv_baseline_geometry(orc, name, prec):
+    cp, stem = BASELINE_LAYERS[name]
+    F, I = rand_inputs(cp, 20177, stem)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    for algo in ALGOS:
+        O = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo=algo, precision=prec))
+        err = per_output_error(O, ref, scale)
+        assert err <= TOL[prec], (name, algo, prec, err, cg.last_path())
+
+
+# ---------------------------------------------------------------- size-independent properties at full size
+def test_full_size_properties():
+    """C2 56x56 64->64 at b=128: batch slicing is exact (each output depends only on
+    its own image), reruns are bitwise deterministic (no float atomics; the
+    reference guarantees the same, gemm.hpp:40-45), and conv is linear in I."""
+    cp = dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=56, w_i=56, b=128, s=1, p=1)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    F = cg.empty_tensor4(64, 3, 3, 64)
+    F.copy_(torch.rand(F.shape, generator=g, device="cuda") * 2 - 1)
+    I = cg.empty_tensor4(56, 56, 64, 128)
+    I.copy_(torch.rand(I.shape, generator=g, device="cuda") * 2 - 1)
+    for prec in ("tf32", "3xtf32"):
+        O1 = cg.conv(F, I, cp, precision=prec)
+        O2 = cg.conv(F, I, cp, precision=prec)
+        assert torch.equal(O1, O2)
+        # image 37 alone
+        cp1 = dict(cp, b=1)
+        I37 = cg.empty_tensor4(56, 56, 64, 1)
+        I37.copy_(I[..., 37:38])
+        O37 = cg.conv(F, I37, cp1, precision=prec)
+        assert torch.equal(O37[..., 0], O1[..., 37])
+    # linearity (within tolerance): conv(F, 2*I) == 2*conv(F, I) exactly (power-of-two scaling)
+    I2 = cg.empty_tensor4(56, 56, 64, 128)
+    I2.copy_(I * 2)
+    O = cg.conv(F, I, cp, precision="3xtf32")
+    assert torch.equal(cg.conv(F, I2, cp, precision="3xtf32"), O * 2)
+
+
+def test_explicit_equals_fused_ffma(orc):
+    """FFMA explicit and fused use the same per-output accumulation order -> bitwise equal
+    (the reference's own fused == explicit property, test_convgemm.cpp:163-190)."""
+    cp = dict(k_n=48, k_h=3, k_w=3, c_i=24, h_i=15, w_i=15, b=3, s=2, p=1)
+    F, I = rand_inputs(cp, 3)
+    a = cg.conv(to_dev(F), to_dev(I), cp, algo="fused", precision="ffma")
+    b = cg.conv(to_dev(F), to_dev(I), cp, algo="explicit", precision="ffma")
+    assert torch.equal(a, b)
+
+
+# ---------------------------------------------------------------- reference call semantics
+def test_host_path_matches_device_path():
+    cp = dict(k_n=32, k_h=3, k_w=3, c_i=16, h_i=20, w_i=18, b=2, s=1, p=1)
+    F, I = rand_inputs(cp, 11)
+    for prec in PRECS:
+        for algo in ALGOS:
+            host = cg.conv(F, I, cp, algo=algo, precision=prec)
+            dev = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo=algo, precision=prec))
+            assert np.array_equal(host, dev), (algo, prec)
+
+
+def test_reference_named_entry_points(orc):
+    cp = cg.ConvParams(k_n=16, k_h=3, k_w=3, c_i=8, h_i=12, w_i=12, b=2, s=1, p=1)
+    F, I = rand_inputs(vars(cp), 40)
+    ref = orc.conv_gemm(F, I, vars(cp))
+    scale = orc.output_scale(F, I, vars(cp))
+    assert per_output_error(cg.conv_gemm(F, I, cp, cg.BlockingParams(), 4), ref, scale) <= 1e-5
+    assert per_output_error(cg.conv_im2col_gemm(F, I, cp), ref, scale) <= 1e-5
+
+
+def test_shape_mismatch_raises():
+    cp = dict(k_n=4, k_h=3, k_w=3, c_i=2, h_i=8, w_i=8, b=1, s=1, p=1)
+    F, I = rand_inputs(cp, 1)
+    with pytest.raises(cg.InvalidGeometry):
+        cg.conv(to_dev(F), to_dev(I[:, :, :1, :]), cp)
+    with pytest.raises(cg.InvalidGeometry):
+        cg.conv(F, I, dict(cp, h_i=2, w_i=2, p=0))
+
+
+def test_workspace_limit_kills_explicit_not_fused(orc):
+    """test_convgemm.cpp:231-242 on the device: under a workspace limit the explicit path
+    fails with AllocationFailure while the fused path (no HBM B-hat) still runs."""
+    cp = dict(k_n=192, k_h=5, k_w=5, c_i=64, h_i=55, w_i=55, b=1, s=1, p=0)
+    F, I = rand_inputs(cp, 39)
+    cg.lib.cgb_scratch_release()
+    cg.scratch_set_limit(9 << 20)
+    try:
+        with pytest.raises(cg.AllocationFailure):
+            cg.conv(to_dev(F), to_dev(I), cp, algo="explicit", precision="tf32")
+        O = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo="fused", precision="tf32"))
+    finally:
+        cg.scratch_set_limit(0)
+    ref = orc.conv_gemm(F, I, cp)
+    assert per_output_error(O, ref, orc.output_scale(F, I, cp)) <= 5e-3
+
+
+def test_kernels_actually_launch():
+    n0 = cg.kernel_launch_count()
+    cp = dict(k_n=8, k_h=1, k_w=1, c_i=8, h_i=4, w_i=4, b=1, s=1, p=0)
+    F, I = rand_inputs(cp, 2)
+    cg.conv(to_dev(F), to_dev(I), cp)
+    torch.cuda.synchronize()
+    assert cg.kernel_launch_count() > n0
