@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 convolution operator on BASELINE.json configs[1].
+
+Workload (one "step"): the seven ResNet-50 v1.5 3x3 convolutions of BASELINE.json
+configs[1] at b=128 per GPU -- 56^2 64->64, 28^2 128->128, 14^2 256->256, 7^2 512->512
+(stride 1, pad 1) and the stride-2 variants 56->28 c128, 28->14 c256, 14->7 c512 --
+each run once through the fused operator (cgb_conv, CGB_ALGO_FUSED), FP32 tensors in
+the reference layouts, synthetic uniform[-1,1] inputs from a fixed seed.
+
+metric/unit: BASELINE.json's "conv GFLOPS (2*k_n*h_o*w_o*b*k_h*k_w*c_i/s)"; value =
+whole-job FLOPs / max-over-ranks device time. The headline precision is TF32 (the mode
+the north-star roofline target is stated in, tolerance 5e-3); the fp32-accurate 3xTF32
+mode is measured in the same run and reported under "modes".
+
+Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun, one rank
+per GPU, batch sharded with no collective in the timed region; filters broadcast once).
+--impl reference times the reference's own CPU conv_gemm (oracle/_ref) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "conv GFLOPS (2·k_n·h_o·w_o·b·k_h·k_w·c_i/s) per layer & % TF32 TC roofline"
+UNIT = "GFLOPS"
+BATCH = 128
+
+# (name, k_n, k, c_i, h_i, s, p)  -- BASELINE.json configs[1]
+LAYERS = [
+    ("r50_3x3_56_64", 64, 3, 64, 56, 1, 1),
+    ("r50_3x3_28_128", 128, 3, 128, 28, 1, 1),
+    ("r50_3x3_14_256", 256, 3, 256, 14, 1, 1),
+    ("r50_3x3_7_512", 512, 3, 512, 7, 1, 1),
+    ("r50_3x3_s2_56_128", 128, 3, 128, 56, 2, 1),
+    ("r50_3x3_s2_28_256", 256, 3, 256, 28, 2, 1),
+    ("r50_3x3_s2_14_512", 512, 3, 512, 14, 2, 1),
+]
+
+
+def layer_cp(layer, b):
+    name, k_n, k, c_i, h_i, s, p = layer
+    return dict(k_n=k_n, k_h=k, k_w=k, c_i=c_i, h_i=h_i, w_i=h_i, b=b, s=s, p=p)
+
+
+def out_hw(cp):
+    return (cp["h_i"] - cp["k_h"] + 2 * cp["p"]) // cp["s"] + 1, (cp["w_i"] - cp["k_w"] + 2 * cp["p"]) // cp["s"] + 1
+
+
+def flops(cp):
+    h_o, w_o = out_hw(cp)
+    return 2 * cp["k_n"] * h_o * w_o * cp["b"] * cp["k_h"] * cp["k_w"] * cp["c_i"]
+
+
+def nbytes(cp):
+    h_o, w_o = out_hw(cp)
+    return 4 * (cp["h_i"] * cp["w_i"] * cp["c_i"] * cp["b"] + cp["k_n"] * cp["k_h"] * cp["k_w"] * cp["c_i"]
+                + cp["k_n"] * h_o * w_o * cp["b"])
+
+
+def split_range(count, rank, nranks):
+    """threads.hpp:20-25: contiguous static split, first count % nranks ranks get +1."""
+    base, rem = divmod(count, nranks)
+    begin = rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)
+
+
+def peaks():
+    p = {"hbm_gbs": 6545.6, "bf16_tflops": 1627.7, "src": "MEASURED_PEAKS.json"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p["hbm_gbs"] = float(m["hbm_gbs"])
+        p["bf16_tflops"] = float(m["bf16_tflops"])
+    except Exception:
+        p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
+    p["tf32_tflops"] = p["bf16_tflops"] / 2.0  # dense TF32 = 1/2 dense BF16 on tcgen05
+    return p
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def cpu_reference_time(batch_sample, min_time, threads, rng_seed=20177):
+    """The reference's own conv_gemm<float> (oracle/_ref, compiled from /root/reference)
+    timed with its repeat-until-min_time loop (proj/src/bench.cpp:200-210)."""
+    import numpy as np
+    from oracle.oracle import REFERENCE_SO, Reference, Restatement
+    kind = "reference"
+    try:
+        ref = Reference()
+        run = lambda F, I, cp: ref.conv_gemm(F, I, cp, threads=threads)  # noqa: E731
+    except Exception:
+        kind = "port"
+        orc = Restatement()
+        run = lambda F, I, cp: orc.conv_gemm(F, I, cp)  # noqa: E731
+    rng = np.random.default_rng(rng_seed)
+    total_flops, total_t = 0, 0.0
+    for layer in LAYERS:
+        cp = layer_cp(layer, batch_sample)
+        F = np.asfortranarray(rng.uniform(-1, 1, (cp["k_n"], 3, 3, cp["c_i"])).astype(np.float32))
+        I = np.asfortranarray(rng.uniform(-1, 1, (cp["h_i"], cp["w_i"], cp["c_i"], cp["b"])).astype(np.float32))
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            run(F, I, cp)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= min_time:
+                break
+        total_flops += flops(cp) * reps
+        total_t += el
+    return total_flops / total_t / 1e9, kind, total_t
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    sample_b = args.ref_batch
+    # warm-up steps
+    for _ in range(args.warmup):
+        cpu_reference_time(sample_b, 0.0, threads)
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        v, kind, t = cpu_reference_time(sample_b, 0.0, threads)
+        vals.append(v)
+        t_all += t
+    value = statistics.mean(vals)
+    step_flops = sum(flops(layer_cp(l, sample_b)) for l in LAYERS)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "ResNet-50 v1.5 3x3 convs (BASELINE configs[1])", "global_batch": BATCH,
+                   "layers": [l[0] for l in LAYERS], "algo": "conv_gemm (reference fused ConvGemm)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"each step = the 7 layers at b={sample_b} (of {BATCH}), "
+                                   f"{step_flops / 1e9:.1f} GFLOP, conv_gemm<float> threads={threads}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def make_layer_tensors(cg, torch, layers, b, rank, world, seed=20177):
+    out = []
+    g = torch.Generator(device="cuda").manual_seed(seed + 1000 * rank)
+    for layer in layers:
+        cp = layer_cp(layer, b)
+        h_o, w_o = out_hw(cp)
+        F = cg.empty_tensor4(cp["k_n"], 3, 3, cp["c_i"])
+        gf = torch.Generator(device="cuda").manual_seed(seed + hash(layer[0]) % 1000)
+        F.copy_(torch.rand(F.shape, generator=gf, device="cuda") * 2 - 1)
+        if world > 1:
+            import torch.distributed as dist
+            dist.broadcast(F, src=0)  # filters broadcast once, outside the timed region
+        I = cg.empty_tensor4(cp["h_i"], cp["w_i"], cp["c_i"], b)
+        I.copy_(torch.rand(I.shape, generator=g, device="cuda") * 2 - 1)
+        O = cg.empty_tensor4(cp["k_n"], h_o, w_o, b)
+        out.append((layer, cp, F, I, O))
+    return out
+
+
+def time_mode(cg, torch, tensors, precision, steps, warmup, flush, world):
+    st = torch.cuda.current_stream()
+    nl = len(tensors)
+    for _ in range(warmup):
+        for layer, cp, F, I, O in tensors:
+            cg.conv(F, I, cp, algo="fused", precision=precision, out=O)
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
+          for _ in range(steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    launches0 = cg.kernel_launch_count()
+    for s in range(steps):
+        flush.zero_()  # L2 flush (256 MiB write) between timed steps, outside the events
+        for li, (layer, cp, F, I, O) in enumerate(tensors):
+            ev[s][li][0].record(st)
+            cg.conv(F, I, cp, algo="fused", precision=precision, out=O)
+            ev[s][li][1].record(st)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = cg.kernel_launch_count() - launches0
+    per_layer = [[ev[s][li][0].elapsed_time(ev[s][li][1]) for s in range(steps)] for li in range(nl)]
+    step_ms = [sum(per_layer[li][s] for li in range(nl)) for s in range(steps)]
+    return per_layer, step_ms, launches
+
+
+def time_e2e(cg, torch, tensors, precision, steps, warmup, world):
+    """Public host-buffer API (cgb_conv_host via cg.conv on numpy arrays backed by
+    pinned memory): H2D of F and I, the kernel, D2H of O, every step."""
+    host = []
+    h2d = d2h = 0
+    for layer, cp, F, I, O in tensors:
+        hF = torch.empty(F.numel(), dtype=torch.float32, pin_memory=True)
+        hI = torch.empty(I.numel(), dtype=torch.float32, pin_memory=True)
+        hO = torch.empty(O.numel(), dtype=torch.float32, pin_memory=True)
+        hF.copy_(F.permute(3, 2, 1, 0).reshape(-1))
+        hI.copy_(I.permute(3, 2, 1, 0).reshape(-1))
+        npF = hF.numpy().reshape(F.shape, order="F")
+        npI = hI.numpy().reshape(I.shape, order="F")
+        npO = hO.numpy().reshape(O.shape, order="F")
+        host.append((cp, npF, npI, npO, (hF, hI, hO)))
+        h2d += 4 * (F.numel() + I.numel())
+        d2h += 4 * O.numel()
+    for _ in range(warmup):
+        for cp, npF, npI, npO, _k in host:
+            cg.conv(npF, npI, cp, algo="fused", precision=precision, out=npO)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    legacy = torch.cuda.default_stream()
+    e0.record(legacy)
+    for _ in range(steps):
+        for cp, npF, npI, npO, _k in host:
+            cg.conv(npF, npI, cp, algo="fused", precision=precision, out=npO)
+    e1.record(legacy)
+    torch.cuda.synchronize()
+    barrier(world)
+    return e0.elapsed_time(e1) / steps, h2d, d2h
+
+
+def run_gpu_arm(args, world, rank, local):
+    import torch
+
+    import paper_2005_06410_b200 as cg
+    torch.cuda.set_device(local)
+    pk = peaks()
+    b = BATCH  # weak scaling: b=128 per GPU (each rank an independent batch shard)
+    if args.scaling == "strong":
+        lo, hi = split_range(BATCH, rank, world)
+        b = hi - lo
+    tensors = make_layer_tensors(cg, torch, LAYERS, b, rank, world)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+
+    modes = {}
+    headline = args.precision
+    order = [headline] + [m for m in ("3xtf32",) if m != headline and not args.quick]
+    for prec in order:
+        if clocks and prec == headline:
+            clocks.start()
+        per_layer, step_ms, launches = time_mode(cg, torch, tensors, prec, args.steps, args.warmup, flush, world)
+        if clocks and prec == headline:
+            clk = clocks.stop()
+        ms_step = statistics.mean(step_ms)
+        ms_step = max_over_ranks(ms_step, world)
+        step_flops_local = sum(flops(cp) for _, cp, _, _, _ in tensors)
+        total_flops = step_flops_local * world if args.scaling == "weak" else \
+            sum(flops(layer_cp(l, BATCH)) for l in LAYERS)
+        layers = []
+        for li, (layer, cp, F, I, O) in enumerate(tensors):
+            t = statistics.mean(per_layer[li]) * 1e-3
+            fl, by = flops(cp), nbytes(cp)
+            t_tc = fl / (pk["tf32_tflops"] * 1e12)
+            t_hbm = by / (pk["hbm_gbs"] * 1e9)
+            layers.append({"layer": layer[0], "ms": round(t * 1e3, 4), "gflops": round(fl / t / 1e9, 1),
+                           "tflops": round(fl / t / 1e12, 1), "hbm_gbs": round(by / t / 1e9, 1),
+                           "bound": "tensor" if t_tc >= t_hbm else "hbm",
+                           "roofline_frac": round(max(t_tc, t_hbm) / t, 4),
+                           "tf32_frac": round(t_tc / t, 4)})
+        kern_s = sum(statistics.mean(per_layer[li]) for li in range(len(tensors))) * 1e-3
+        modes[prec] = {"value": total_flops / (ms_step * 1e-3) / 1e9, "ms_per_step": ms_step,
+                       "layers": layers, "gpu_launches": launches,
+                       "achieved_tflops": step_flops_local / kern_s / 1e12}
+    # e2e through the host-buffer public API (headline precision)
+    e2e_ms, h2d, d2h = time_e2e(cg, torch, tensors, headline, max(1, min(args.steps, 3)), 1, world)
+    e2e_ms = max_over_ranks(e2e_ms, world)
+    if rank != 0:
+        return 0
+    hm = modes[headline]
+    step_flops_local = sum(flops(cp) for _, cp, _, _, _ in tensors)
+    total_flops = step_flops_local * world if args.scaling == "weak" else \
+        sum(flops(layer_cp(l, BATCH)) for l in LAYERS)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, kind, t = cpu_reference_time(args.cpu_batch, args.cpu_min_time, os.cpu_count() or 1)
+        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind,
+               "sample": f"the 7 layers at b={args.cpu_batch} (of {BATCH}), conv_gemm<float> repeated until "
+                         f">= {args.cpu_min_time}s per layer ({t:.1f}s CPU total), threads=nproc"}
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(headline)
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": hm["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": hm["ms_per_step"], "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "tf32" if headline == "tf32" else "f32",
+        "data": "synthetic (uniform[-1,1], seeded torch generator on device)",
+        "config": {"workload": "ResNet-50 v1.5 3x3 convs at b=128 (BASELINE configs[1]), fused operator",
+                   "global_batch": BATCH * world if args.scaling == "weak" else BATCH, "batch_per_gpu": b,
+                   "layers": [l[0] for l in LAYERS], "precision": headline, "algo": "fused",
+                   "l2": "256 MiB L2 flush between timed steps (outside the CUDA events); per-step traffic > L2",
+                   "parallelism": f"batch-sharded dp{world}, no collective in the timed region"},
+        "roofline": {"bound": "tensor", "achieved": hm["achieved_tflops"], "peak": pk["tf32_tflops"],
+                     "unit": "TFLOP/s", "frac": hm["achieved_tflops"] / pk["tf32_tflops"], "traffic": traffic,
+                     "peak_src": f"dense TF32 = bf16_tflops/2 from {pk['src']} (of measured)",
+                     "per_layer": hm["layers"]},
+        "cpu_baseline": cpu,
+        "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "api": "cgb_conv_host (host buffers, pinned)"},
+        "gpu_launches": hm["gpu_launches"],
+        "clocks": clk if clocks else None,
+        "modes": {m: {"value": v["value"], "ms_per_step": v["ms_per_step"],
+                      "tf32_frac": v["achieved_tflops"] / pk["tf32_tflops"],
+                      "per_layer_tflops": {l["layer"]: l["tflops"] for l in v["layers"]}} for m, v in modes.items()},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "3xtf32", "auto"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--quick", action="store_true", help="headline precision only")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-batch", type=int, default=2)
+    ap.add_argument("--cpu-min-time", type=float, default=2.0)
+    ap.add_argument("--ref-batch", type=int, default=2)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    world, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            return run_reference_arm(args, world, rank)
+        return run_gpu_arm(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

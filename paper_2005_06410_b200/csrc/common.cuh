@@ -162,18 +162,24 @@ CGB_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
 CGB_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------ descriptors
-// 128B-swizzle layout type code in bits [61,64) of the smem descriptor.
+// Layout type codes in bits [61,64) of the smem descriptor. kind::tf32 MN-major
+// operands only accept the 128B swizzle with 32-byte atoms (SWIZZLE_128B_BASE32B,
+// verified on B200 by tools/umma_probe.cu); K-major operands use the 16-byte-atom one.
 constexpr uint64_t kLayoutSW128 = 2;
+constexpr uint64_t kLayoutSW128_32B = 1;
 
-// Shared-memory matrix descriptor (sm_100 "version 1"), no base offset.
-CGB_DEV uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t base_offset = 0) {
+// Shared-memory matrix descriptor (sm_100 "version 1"). Swizzling is applied on
+// absolute shared addresses, so a start address shifted by whole 128-byte rows
+// needs base_offset 0 (measured: tools/umma_probe.cu).
+CGB_DEV uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t base_offset = 0,
+                           uint64_t layout = kLayoutSW128) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
   d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
   d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(base_offset & 7u) << 49;
-  d |= kLayoutSW128 << 61;
+  d |= layout << 61;
   return d;
 }
 

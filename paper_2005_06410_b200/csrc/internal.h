@@ -35,7 +35,8 @@ cudaError_t launch_tc_conv(const float* f_hi, const float* f_lo, int64_t ldf, co
                            cudaStream_t st);
 
 // 2-D TMA descriptor over a filter matrix (k_n x K, leading dimension ldf floats):
-// box 32 filters x 32 rows, 128-byte swizzle (the MN-major UMMA B layout).
+// box 32 filters x 32 rows, 128-byte swizzle with 32-byte atoms (the MN-major
+// kind::tf32 UMMA B layout, SWIZZLE_128B_BASE32B).
 cudaError_t make_filter_tmap(CUtensorMap* tm, const float* f, int64_t k_n, int64_t K, int64_t ldf);
 
 // V2: stride/phase "shifted window" tcgen05 kernel; returns cudaErrorNotSupported

@@ -16,7 +16,7 @@
 //     (register-staged: LDG -> [TF32 rounding | 3xTF32 hi/lo split] -> STS into the
 //     canonical swizzled layout). The lowered matrix never reaches HBM on the fused
 //     path; on the explicit path the rows come from B (ld = ldb).
-//   B (K x filters, MN-major, 128B swizzle): TMA boxes of 32 filters x 32 rows
+//   B (K x filters, MN-major, 128B swizzle of 32-byte atoms): TMA boxes of 32 filters x 32 rows
 //     straight from F (k_n fastest is already MN-major), or from the hi/lo split.
 // Roles (320 threads): warps 0-7 A producers (warps 0-3 then run the epilogue on
 // TMEM lanes 0-127), warp 8 TMA producer + TMEM allocator, warp 9 MMA issuer.
@@ -250,13 +250,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           // A: K-major SW128, k-step = +32 B inside the swizzle row; 8-row groups 1024 B apart.
-          // B: MN-major SW128, k-step = +1024 B (8 rows of 128 B); 32-filter blocks 4096 B apart.
+          // B: MN-major SW128 with 32-byte atoms (the only MN-major layout kind::tf32 takes):
+          //    k-step = +1024 B (8 rows of 128 B), 4-row groups 512 B apart, 32-filter blocks 4096 B apart.
           const uint64_t ad = smem_desc(a_hi + kk * 32, 16, 1024);
-          const uint64_t bd = smem_desc(b_hi + kk * 1024, 4096, 1024);
+          const uint64_t bd = smem_desc(b_hi + kk * 1024, 4096, 512, 0, kLayoutSW128_32B);
           const uint32_t acc = (kt | kk) != 0;
           if (SPLIT) {
             const uint64_t ad_lo = smem_desc(smem_u32(a_tile(s, 1)) + kk * 32, 16, 1024);
-            const uint64_t bd_lo = smem_desc(smem_u32(b_tile(s, 1)) + kk * 1024, 4096, 1024);
+            const uint64_t bd_lo = smem_desc(smem_u32(b_tile(s, 1)) + kk * 1024, 4096, 512, 0, kLayoutSW128_32B);
             mma_tf32(tmem_base, ad_lo, bd, idesc, acc);
             mma_tf32(tmem_base, ad, bd_lo, idesc, 1);
             mma_tf32(tmem_base, ad, bd, idesc, 1);
