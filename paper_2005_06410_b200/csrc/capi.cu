@@ -91,6 +91,20 @@ cudaError_t make_filter_tmap(CUtensorMap* tm, const float* f, int64_t k_n, int64
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+cudaError_t make_filter_tmap_tapmajor(CUtensorMap* tm, const float* f, const ConvGeom& g) {
+  auto enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  const int64_t taps = g.k_h * g.k_w;
+  cuuint64_t dims[3] = {(cuuint64_t)g.k_n, (cuuint64_t)taps, (cuuint64_t)g.c_i};
+  cuuint64_t strides[2] = {(cuuint64_t)(g.k_n * 4), (cuuint64_t)(g.k_n * taps * 4)};
+  cuuint32_t box[3] = {32, 1, 32};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(f), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // ------------------------------------------------------------------ workspace (ScratchTracker)
 struct Scratch {
   std::mutex mu;
@@ -277,6 +291,9 @@ cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, con
     if (!Bhat && shifted_supported(g)) {
       e = launch_tc_conv_shifted(f_hi, f_lo, ldf, I, O, g, split, s);
       g_last_path = 5;
+    } else if (!Bhat && gather_supported(g) && ldf == g.k_n) {
+      e = launch_tc_gather(f_hi, f_lo, I, O, g, split, s);
+      g_last_path = 6;
     } else {
       e = launch_tc_conv(f_hi, f_lo, ldf, I, Bhat, pl.ldb, O, g, split, s);
       g_last_path = Bhat ? 2 : 1;

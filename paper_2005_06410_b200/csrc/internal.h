@@ -39,6 +39,15 @@ cudaError_t launch_tc_conv(const float* f_hi, const float* f_lo, int64_t ldf, co
 // kind::tf32 UMMA B layout, SWIZZLE_128B_BASE32B).
 cudaError_t make_filter_tmap(CUtensorMap* tm, const float* f, int64_t k_n, int64_t K, int64_t ldf);
 
+// 3-D TMA descriptor over F seen as (k_n, tap = i_kh + i_kw*k_h, c_i): box 32 filters x
+// 1 tap x 32 channels, 32-byte-atom 128B swizzle. Needs k_n % 4 == 0.
+cudaError_t make_filter_tmap_tapmajor(CUtensorMap* tm, const float* f, const ConvGeom& g);
+
+// K3 tap-major gather kernel (tc_gather.cu): c_i >= 16, k_n % 4 == 0.
+bool gather_supported(const ConvGeom& g);
+cudaError_t launch_tc_gather(const float* f_hi, const float* f_lo, const float* I, float* O, const ConvGeom& g,
+                             bool split, cudaStream_t st);
+
 // V2: stride/phase "shifted window" tcgen05 kernel; returns cudaErrorNotSupported
 // when the geometry is outside its domain (caller falls back to launch_tc_conv).
 bool shifted_supported(const ConvGeom& g);
