@@ -125,6 +125,10 @@ uint64_t cgb_kernel_launch_count(void);
 /* Kernel path the last cgb_conv chose on this thread: 0 none, 1 tcgen05 implicit,
  * 2 tcgen05 explicit, 3 ffma implicit, 4 ffma explicit. */
 int cgb_last_path(void);
+/* Profiling hook: per-CTA MMA-issuer cycle counters of the last shifted-window launch
+ * made with CGB_DEBUG_SW & 64 set (8 uint64 per CTA: total, wait accumulator,
+ * wait A window, wait filter tile, tiles). Returns 0 on success. */
+int cgb_debug_sw_stats(unsigned long long* host, int n_cta);
 
 #ifdef __cplusplus
 }

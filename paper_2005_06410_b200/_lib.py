@@ -18,7 +18,7 @@ SYMBOLS = (
     "cgb_conv_workspace_bytes", "cgb_conv", "cgb_conv_gemm", "cgb_conv_im2col_gemm", "cgb_im2col",
     "cgb_conv_host", "cgb_scratch_current_bytes", "cgb_scratch_peak_bytes", "cgb_scratch_reset_peak",
     "cgb_scratch_set_limit", "cgb_scratch_release", "cgb_last_error", "cgb_version",
-    "cgb_kernel_launch_count", "cgb_last_path",
+    "cgb_kernel_launch_count", "cgb_last_path", "cgb_debug_sw_stats",
 )
 
 
@@ -61,6 +61,7 @@ def _load() -> ctypes.CDLL:
         "cgb_version": (ctypes.c_char_p, []),
         "cgb_kernel_launch_count": (ctypes.c_uint64, []),
         "cgb_last_path": (ctypes.c_int, []),
+        "cgb_debug_sw_stats": (ctypes.c_int, [vp, ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -288,9 +288,13 @@ cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, con
     g_last_path = Bhat ? 4 : 3;
   } else {
     const bool split = prec == CGB_PREC_3XTF32;
-    if (!Bhat && shifted_supported(g)) {
+    e = cudaErrorNotSupported;
+    if (!Bhat && shifted_supported(g) && ldf == g.k_n) {
       e = launch_tc_conv_shifted(f_hi, f_lo, ldf, I, O, g, split, s);
       g_last_path = 5;
+    }
+    if (e != cudaErrorNotSupported) {
+      // launched (or failed for real)
     } else if (!Bhat && gather_supported(g) && ldf == g.k_n) {
       e = launch_tc_gather(f_hi, f_lo, I, O, g, split, s);
       g_last_path = 6;

@@ -51,6 +51,17 @@ CGB_DEV float to_tf32(float x) {
   return __uint_as_float(r);
 }
 
+// TF32 split by truncation (the tensor core ignores the low 13 mantissa bits of a
+// kind::tf32 operand): hi keeps the top 10 mantissa bits, lo = x - hi is exact in fp32.
+CGB_DEV float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// 32-byte vector store (sm_100 STG.256).
+CGB_DEV void st_global_v8(float* p, const uint32_t* r) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
 // ------------------------------------------------------------------ mbarrier
 CGB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -76,6 +87,14 @@ CGB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra CGB_WAIT;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Warp-cooperative wait: one lane polls the mbarrier, the others park at __syncwarp
+// (32 pollers per warp otherwise compete with the tensor core for shared-memory
+// bandwidth). Memory ordering: the polling lane's acquire + __syncwarp.
+CGB_DEV void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
 }
 
 // cp.async (LDGSTS) completion tracked by an mbarrier: one arrival per thread

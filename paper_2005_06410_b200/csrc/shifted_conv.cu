@@ -23,6 +23,7 @@
 // Roles (448 threads): warps 0-7 A producers, warp 8 filter TMA + TMEM alloc,
 // warp 9 MMA issue, warps 10-13 epilogue (TMEM lanes 64*... per warp%4).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -38,6 +39,9 @@ constexpr int THREADS = 14 * 32;
 
 struct Args {
   int32_t k_n, k_h, k_w, c_i, h_i, w_i, p, h_o, w_o, b;
+  int32_t s;          // stride: the window is split into s*s phase planes (polyphase)
+  int32_t nph_h, nph_w, NPH;  // phases used: min(s, k_h) x min(s, k_w)
+  int32_t R_pad;      // staged rows per phase rounded to 8 (phase stride in a slot = R_pad*128 B)
   int32_t Hq, Wq;     // padded plane
   int32_t dmax;       // (k_h-1) + Hq*(k_w-1)
   int32_t R;          // staged rows per chunk = MT*128 + dmax
@@ -45,7 +49,11 @@ struct Args {
   int32_t taps;
   int32_t m_tiles, n_tiles;
   int64_t Mp;         // padded output rows Hq*Wq*b
+  int32_t Mp32;       // same, 32-bit (shifted_supported guarantees < 2^31 - tile)
   int64_t plane;      // h_i*w_i
+  unsigned long long* stats;  // per-CTA cycle counters when dbg & 64 (profiling only)
+  int32_t dbg;        // profiling switches (CGB_DEBUG_SW): 1 = producers skip loads, 2 = skip MMAs,
+                      //   4 = skip epilogue stores, 8 = skip filter TMA
 };
 
 template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES>
@@ -114,50 +122,72 @@ __global__ void __launch_bounds__(THREADS, 1)
     // consecutive padded pixels -> coalesced reads per channel), 32 channels per row.
     const int row_blocks = (a.R + 31) / 32;
     const int32_t hw_q = a.Hq * a.Wq;
+    const int32_t plane = (int32_t)a.plane;
     int it = 0;  // chunk counter across tiles (slot ring position)
+    // one row block = 32 consecutive padded pixels (lane = row) x 32 channels
+    auto row_src = [&](int32_t row, int32_t ph_a, int32_t ph_c, int32_t m0, int cc, bool& ok) -> const float* {
+      const int32_t Q = m0 + row;
+      ok = row < a.R && Q < a.Mp32;
+      if (!ok) return I;
+      const int32_t bb = Q / hw_q;
+      const int32_t rem = Q - bb * hw_q;
+      const int32_t wq = rem / a.Hq, hq = rem - wq * a.Hq;
+      const int32_t h = a.s * hq + ph_a - a.p, w = a.s * wq + ph_c - a.p;
+      ok = (unsigned)h < (unsigned)a.h_i && (unsigned)w < (unsigned)a.w_i;
+      return I + ((int64_t)bb * a.c_i + (int64_t)cc * BK) * a.plane + (w * a.h_i + h);
+    };
+    auto load_rows = [&](const float* src, bool ok, int cmax, float (&v)[BK]) {
+      if (cmax >= BK) {
+#pragma unroll
+        for (int c = 0; c < BK; ++c) v[c] = ok ? __ldg(src + c * plane) : 0.0f;
+      } else {
+#pragma unroll
+        for (int c = 0; c < BK; ++c) v[c] = (ok && c < cmax) ? __ldg(src + c * plane) : 0.0f;
+      }
+    };
+    auto store_rows = [&](int32_t row, const float (&v)[BK], uint8_t* dst_hi, uint8_t* dst_lo) {
+      if (row >= a.R) return;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint32_t off = row * 128 + ((ch ^ (row & 7)) << 4);
+        if (SPLIT) {
+          float4 hi, lo;
+          hi.x = tf32_trunc(v[4 * ch + 0]); lo.x = v[4 * ch + 0] - hi.x;
+          hi.y = tf32_trunc(v[4 * ch + 1]); lo.y = v[4 * ch + 1] - hi.y;
+          hi.z = tf32_trunc(v[4 * ch + 2]); lo.z = v[4 * ch + 2] - hi.z;
+          hi.w = tf32_trunc(v[4 * ch + 3]); lo.w = v[4 * ch + 3] - hi.w;
+          *reinterpret_cast<float4*>(dst_hi + off) = hi;
+          *reinterpret_cast<float4*>(dst_lo + off) = lo;
+        } else {
+          *reinterpret_cast<float4*>(dst_hi + off) =
+              make_float4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+        }
+      }
+    };
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const int64_t m0 = (int64_t)(tile % a.m_tiles) * (MT * 128);
+      const int32_t m0 = (tile % a.m_tiles) * (MT * 128);
       for (int cc = 0; cc < a.CC; ++cc, ++it) {
         const int s = it % A_SLOTS;
         const uint32_t ph = (it / A_SLOTS) & 1;
         mbar_wait(&a_empty[s], ph ^ 1);
         uint8_t* dst_hi = a_slot(s, 0);
         uint8_t* dst_lo = a_slot(s, SPLIT ? 1 : 0);
-        for (int rb = warp; rb < row_blocks; rb += PRODUCER_WARPS) {
-          const int row = rb * 32 + lane;
-          const int64_t Q = m0 + row;
-          bool ok = row < a.R && Q < a.Mp;
-          const float* src = I;
-          if (ok) {
-            const int32_t bb = (int32_t)(Q / hw_q);
-            const int32_t rem = (int32_t)(Q - (int64_t)bb * hw_q);
-            const int32_t wq = rem / a.Hq, hq = rem - wq * a.Hq;
-            const int32_t h = hq - a.p, w = wq - a.p;
-            ok = (unsigned)h < (unsigned)a.h_i && (unsigned)w < (unsigned)a.w_i;
-            src = I + ((int64_t)bb * a.c_i + (int64_t)cc * BK) * a.plane + (int64_t)w * a.h_i + h;
-          }
-          const int cmax = a.c_i - cc * BK;  // channels available in this chunk
-          float v[BK];
-#pragma unroll
-          for (int c = 0; c < BK; ++c) v[c] = (ok && c < cmax) ? __ldg(src + c * a.plane) : 0.0f;
-          if (row < a.R) {
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-              const uint32_t off = row * 128 + ((ch ^ (row & 7)) << 4);
-              float4 hi, lo;
-              float* h = &hi.x;
-              float* l = &lo.x;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float x = v[4 * ch + e];
-                const float t = to_tf32(x);
-                h[e] = t;
-                if (SPLIT) l[e] = to_tf32(x - t);
-              }
-              *reinterpret_cast<float4*>(dst_hi + off) = hi;
-              if (SPLIT) *reinterpret_cast<float4*>(dst_lo + off) = lo;
-            }
-          }
+        const int cmax = a.c_i - cc * BK;
+        // units = (phase, row block); two units in flight per iteration (64 loads per thread)
+        const int units = a.NPH * row_blocks;
+        for (int u = warp; u < units && !(a.dbg & 1); u += 2 * PRODUCER_WARPS) {
+          const int u2 = u + PRODUCER_WARPS;
+          const int ph0 = u / row_blocks, rb0 = u - ph0 * row_blocks;
+          const int ph1 = u2 / row_blocks, rb1 = u2 - ph1 * row_blocks;
+          bool ok0, ok1;
+          const float* s0 = row_src(rb0 * 32 + lane, ph0 % a.nph_h, ph0 / a.nph_h, m0, cc, ok0);
+          const float* s1 = row_src(rb1 * 32 + lane, ph1 % a.nph_h, ph1 / a.nph_h, m0, cc, ok1);
+          ok1 = ok1 && u2 < units;
+          float v0[BK], v1[BK];
+          load_rows(s0, ok0, cmax, v0);
+          load_rows(s1, ok1, cmax, v1);
+          store_rows(rb0 * 32 + lane, v0, dst_hi + ph0 * a.R_pad * 128, dst_lo + ph0 * a.R_pad * 128);
+          if (u2 < units) store_rows(rb1 * 32 + lane, v1, dst_hi + ph1 * a.R_pad * 128, dst_lo + ph1 * a.R_pad * 128);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -176,6 +206,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int s = it % B_STAGES;
             const uint32_t ph = (it / B_STAGES) & 1;
             mbar_wait(&b_empty[s], ph ^ 1);
+            if (a.dbg & 8) {
+              mbar_arrive(&b_full[s]);
+              continue;
+            }
             mbar_arrive_expect_tx(&b_full[s], bytes);
 #pragma unroll
             for (int j = 0; j < BN / 32; ++j) {
@@ -190,100 +224,117 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- MMA issue
     constexpr uint32_t idesc = idesc_tf32(C::UMMA_N, false, true);
     if (elect_one()) {
+      // Descriptors are built once per operand slot; per UMMA only the 14-bit start
+      // address field moves (row shift d*128 B = d*8 units, k-step 32 B = 2 units,
+      // m-subtile 128 rows = 1024 units, B k-step 1024 B = 64 units, 32-filter block
+      // 4096 B = 256 units), so each issue is an add on a uniform register.
       int ait = 0, bit = 0, t = 0;
+      unsigned long long w_t = 0, w_a = 0, w_b = 0, t_start = clock64();
+      const bool st = (a.dbg & 64) != 0;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++t) {
         const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
         const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
+        unsigned long long c0 = st ? clock64() : 0;
         mbar_wait(&t_empty[acc_set], acc_ph ^ 1);
+        if (st) w_t += clock64() - c0;
         tc_fence_after();
         const uint32_t d_base = tmem_base + acc_set * C::ACC_COLS;
         for (int cc = 0; cc < a.CC; ++cc, ++ait) {
           const int as = ait % A_SLOTS;
+          unsigned long long c1 = st ? clock64() : 0;
           mbar_wait(&a_full[as], (ait / A_SLOTS) & 1);
+          if (st) w_a += clock64() - c1;
           tc_fence_after();
-          const uint32_t a_hi = smem_u32(a_slot(as, 0));
-          const uint32_t a_lo = smem_u32(a_slot(as, SPLIT ? 1 : 0));
-          for (int tap = 0; tap < a.taps; ++tap, ++bit) {
-            const int bs = bit % B_STAGES;
-            mbar_wait(&b_full[bs], (bit / B_STAGES) & 1);
-            tc_fence_after();
-            const int kh = tap % a.k_h, kw = tap / a.k_h;
-            const uint32_t d_rows = kh + a.Hq * kw;
-            const uint32_t b_hi = smem_u32(b_slot(bs, 0));
-            const uint32_t b_lo = smem_u32(b_slot(bs, SPLIT ? 1 : 0));
+          const uint64_t a_hi0 = smem_desc(smem_u32(a_slot(as, 0)), 16, 1024);
+          const uint64_t a_lo0 = smem_desc(smem_u32(a_slot(as, SPLIT ? 1 : 0)), 16, 1024);
+          for (int kw = 0; kw < a.k_w; ++kw)
+            for (int kh = 0; kh < a.k_h; ++kh, ++bit) {
+              const int bs = bit % B_STAGES;
+              unsigned long long c2 = st ? clock64() : 0;
+              mbar_wait(&b_full[bs], (bit / B_STAGES) & 1);
+              if (st) w_b += clock64() - c2;
+              tc_fence_after();
+              // phase (kh % s, kw % s) plane, shifted by kh/s rows + Hq*(kw/s) rows
+              const int phase = (kh % a.s) + a.nph_h * (kw % a.s);
+              const uint64_t shift = (uint64_t)((phase * a.R_pad + kh / a.s + a.Hq * (kw / a.s)) * 8);
+              const uint64_t at = a_hi0 + shift, at_lo = a_lo0 + shift;
+              const uint64_t bt = smem_desc(smem_u32(b_slot(bs, 0)), 4096, 512, 0, kLayoutSW128_32B);
+              const uint64_t bt_lo =
+                  smem_desc(smem_u32(b_slot(bs, SPLIT ? 1 : 0)), 4096, 512, 0, kLayoutSW128_32B);
+              const uint32_t first = (cc == 0 && kw == 0 && kh == 0) ? 0u : 1u;
+              if (!(a.dbg & 2)) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
+                for (int kk = 0; kk < BK / 8; ++kk)
 #pragma unroll
-              for (int hf = 0; hf < BN / C::UMMA_N; ++hf) {
-                const uint32_t boff = hf * (C::UMMA_N / 32) * 4096 + kk * 1024;
-                const uint64_t bd = smem_desc(b_hi + boff, 4096, 512, 0, kLayoutSW128_32B);
-                const uint64_t bd_lo = SPLIT ? smem_desc(b_lo + boff, 4096, 512, 0, kLayoutSW128_32B) : 0;
+                  for (int hf = 0; hf < BN / C::UMMA_N; ++hf)
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                  const uint32_t aoff = (mt * 128 + d_rows) * 128 + kk * 32;
-                  const uint64_t ad = smem_desc(a_hi + aoff, 16, 1024);
-                  const uint32_t d = d_base + mt * BN + hf * C::UMMA_N;
-                  const uint32_t acc = (cc | tap | kk) != 0;
-                  if (SPLIT) {
-                    const uint64_t ad_lo = smem_desc(a_lo + aoff, 16, 1024);
-                    mma_tf32(d, ad_lo, bd, idesc, acc);
-                    mma_tf32(d, ad, bd_lo, idesc, 1);
-                    mma_tf32(d, ad, bd, idesc, 1);
-                  } else {
-                    mma_tf32(d, ad, bd, idesc, acc);
-                  }
-                }
+                    for (int mt = 0; mt < MT; ++mt) {
+                      const uint64_t ad = at + (uint64_t)(mt * 1024 + kk * 2);
+                      const uint64_t bd = bt + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
+                      const uint32_t d = d_base + mt * BN + hf * C::UMMA_N;
+                      const uint32_t acc = kk == 0 ? first : 1u;
+                      if (SPLIT) {
+                        const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024 + kk * 2);
+                        const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
+                        mma_tf32(d, ad_lo, bd, idesc, acc);
+                        mma_tf32(d, ad, bd_lo, idesc, 1);
+                        mma_tf32(d, ad, bd, idesc, 1);
+                      } else {
+                        mma_tf32(d, ad, bd, idesc, acc);
+                      }
+                    }
               }
+              if (a.dbg & 32) mbar_arrive(&b_empty[bs]);
+              else mma_commit(&b_empty[bs]);
             }
-            mma_commit(&b_empty[bs]);
-          }
           mma_commit(&a_empty[as]);
         }
         mma_commit(&t_full[acc_set]);
       }
+      if (st) {
+        unsigned long long* o = a.stats + blockIdx.x * 8;
+        o[0] = clock64() - t_start; o[1] = w_t; o[2] = w_a; o[3] = w_b; o[4] = t;
+      }
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int ew = warp - EPI_WARP0;      // 0..3
-    const int sub = warp % 4;             // TMEM lane quadrant this warp may access
+    const int sub = warp % 4;  // TMEM lane quadrant this warp may access
     const int32_t hw_q = a.Hq * a.Wq;
-    const bool vec = (a.k_n % 4) == 0;
+    const bool vec = (a.k_n % 8) == 0;
     int t = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++t) {
       const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
       const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
-      const int64_t m0 = (int64_t)(tile % a.m_tiles) * (MT * 128);
+      const int32_t m0 = (tile % a.m_tiles) * (MT * 128);
       const int n0 = (tile / a.m_tiles) * BN;
-      mbar_wait(&t_full[acc_set], acc_ph);
+      mbar_wait_warp(&t_full[acc_set], acc_ph);
       tc_fence_after();
 #pragma unroll 1
-      for (int mt = 0; mt < MT; ++mt) {
-        const int64_t Q = m0 + mt * 128 + sub * 32 + lane;
+      for (int mt = 0; mt < MT && !(a.dbg & 16); ++mt) {
+        const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
         int64_t P = -1;
-        if (Q < a.Mp) {
-          const int32_t bb = (int32_t)(Q / hw_q);
-          const int32_t rem = (int32_t)(Q - (int64_t)bb * hw_q);
+        if (Q < a.Mp32) {
+          const int32_t bb = Q / hw_q;
+          const int32_t rem = Q - bb * hw_q;
           const int32_t wq = rem / a.Hq, hq = rem - wq * a.Hq;
-          if (hq < a.h_o && wq < a.w_o) P = hq + (int64_t)a.h_o * (wq + (int64_t)a.w_o * bb);
+          if (hq < a.h_o && wq < a.w_o) P = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
         }
+        const uint32_t trow = tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS + mt * BN;
 #pragma unroll 1
-        for (int cb = 0; cb < BN / 32; ++cb) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS + mt * BN + cb * 32,
-                             r);
+        for (int cb = 0; cb < BN / 64 + (BN % 64 ? 1 : 0); ++cb) {
+          uint32_t r[64];
+          tmem_ld_32x32b_x32(trow + cb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          if (BN >= 64) tmem_ld_32x32b_x32(trow + cb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           tmem_ld_wait();
-          const int nb = n0 + cb * 32;
-          if (P >= 0 && nb < a.k_n) {
+          const int nb = n0 + cb * 64;
+          if (P >= 0 && !(a.dbg & 4)) {
             float* dst = O + P * a.k_n + nb;
-            if (vec && nb + 32 <= a.k_n) {
+            if (vec && nb + 64 <= a.k_n) {
 #pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(dst + j) =
-                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                __uint_as_float(r[j + 3]));
+              for (int j = 0; j < 64; j += 8) st_global_v8(dst + j, &r[j]);
             } else {
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
+              for (int j = 0; j < (BN >= 64 ? 64 : 32); ++j)
                 if (nb + j < a.k_n) dst[j] = __uint_as_float(r[j]);
             }
           }
@@ -292,7 +343,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&t_empty[acc_set]);
-      (void)ew;
     }
   }
   tc_fence_before();
@@ -309,7 +359,8 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
                        cudaStream_t st) {
   using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES>;
   a.R = MT * 128 + a.dmax;
-  const uint32_t a_slot_bytes = (uint32_t)(((a.R + 7) / 8) * 8 * 128);
+  a.R_pad = (a.R + 7) / 8 * 8;
+  const uint32_t a_slot_bytes = (uint32_t)(a.NPH * a.R_pad * 128);
   const size_t smem = (size_t)A_SLOTS * C::NS * a_slot_bytes + (size_t)B_STAGES * C::NS * C::B_TILE + 1024 + 256;
   if (smem > 227 * 1024) return cudaErrorNotSupported;
   a.m_tiles = (int32_t)((a.Mp + MT * 128 - 1) / (MT * 128));
@@ -326,33 +377,103 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   return cudaGetLastError();
 }
 
+static unsigned long long* g_stats = nullptr;
+
 static Args make_args(const ConvGeom& g) {
   Args a;
   a.k_n = (int32_t)g.k_n; a.k_h = (int32_t)g.k_h; a.k_w = (int32_t)g.k_w; a.c_i = (int32_t)g.c_i;
   a.h_i = (int32_t)g.h_i; a.w_i = (int32_t)g.w_i; a.p = (int32_t)g.p; a.h_o = (int32_t)g.h_o;
   a.w_o = (int32_t)g.w_o; a.b = (int32_t)g.b;
-  a.Hq = (int32_t)(g.h_o + g.k_h - 1);
-  a.Wq = (int32_t)(g.w_o + g.k_w - 1);
-  a.dmax = (a.k_h - 1) + a.Hq * (a.k_w - 1);
+  a.s = (int32_t)g.s;
+  a.nph_h = (int32_t)std::min(g.s, g.k_h);
+  a.nph_w = (int32_t)std::min(g.s, g.k_w);
+  a.NPH = a.nph_h * a.nph_w;
+  a.Hq = (int32_t)(g.h_o + (g.k_h - 1) / g.s);
+  a.Wq = (int32_t)(g.w_o + (g.k_w - 1) / g.s);
+  a.dmax = (a.k_h - 1) / a.s + a.Hq * ((a.k_w - 1) / a.s);
   a.CC = (a.c_i + BK - 1) / BK;
   a.taps = a.k_h * a.k_w;
   a.Mp = (int64_t)a.Hq * a.Wq * g.b;
+  a.Mp32 = (int32_t)a.Mp;
   a.plane = g.h_i * g.w_i;
   a.R = 0; a.m_tiles = 0; a.n_tiles = 0;
+  const char* dbg = getenv("CGB_DEBUG_SW");
+  a.dbg = dbg ? atoi(dbg) : 0;
+  a.stats = nullptr;
+  if (a.dbg & 64) {
+    if (!g_stats) cudaMalloc(&g_stats, 1024 * 8 * sizeof(unsigned long long));
+    a.stats = g_stats;
+  }
   return a;
 }
 
 }  // namespace sw
 
-// Domain: stride 1, filters through the tap-major TMA map (k_n % 4 == 0), enough
-// channels per chunk to be worth a window, and little garbage from the padded plane.
-bool shifted_supported(const ConvGeom& g) {
-  if (g.s != 1 || g.k_n % 4 != 0 || g.c_i < 16 || g.k_n > 256) return false;
-  const double waste = (double)((g.h_o + g.k_h - 1) * (g.w_o + g.k_w - 1)) / (double)(g.h_o * g.w_o);
-  if (waste > 1.2) return false;
-  const int64_t dmax = (g.k_h - 1) + (g.h_o + g.k_h - 1) * (g.k_w - 1);
-  return dmax <= 512;
+// Domain: filters through the tap-major TMA map (k_n % 4 == 0), at least half a channel
+// chunk, stride <= 2 (<= 4 phase planes), and a padded plane that wastes < 70% rows.
+static double padded_waste(const ConvGeom& g) {
+  const double hq = (double)(g.h_o + (g.k_h - 1) / g.s), wq = (double)(g.w_o + (g.k_w - 1) / g.s);
+  return hq * wq / (double)(g.h_o * g.w_o);
 }
+
+bool shifted_supported(const ConvGeom& g) {
+  if (g.s > 2 || g.k_n % 4 != 0 || g.c_i < 16) return false;
+  if (padded_waste(g) > 1.7) return false;
+  const int64_t hq = g.h_o + (g.k_h - 1) / g.s, wq = g.w_o + (g.k_w - 1) / g.s;
+  const int64_t dmax = (g.k_h - 1) / g.s + hq * ((g.k_w - 1) / g.s);
+  const int64_t mp = hq * wq * g.b;
+  return dmax <= 256 && mp < (int64_t(1) << 30) && g.c_i * g.h_i * g.w_i * g.b < (int64_t(1) << 31);
+}
+
+namespace sw {
+// Try tile configurations from the largest M tile down; a config is skipped when its
+// shared memory does not fit (launch_cfg -> cudaErrorNotSupported) or when it would
+// leave most SMs idle (fewer tiles than SMs while a smaller M tile exists).
+#define CGB_SW_TRY(MT, BN, SPLIT, AS, BS)                                                   \
+  if (mt_max >= MT) {                                                                       \
+    cudaError_t e_ = launch_cfg<MT, BN, SPLIT, AS, BS>(th, tl, I, O, a, st);               \
+    if (e_ != cudaErrorNotSupported) return e_;                                             \
+  }
+
+static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, const Args& a,
+                            bool split, int sms, cudaStream_t st) {
+  const int bn = a.k_n <= 64 ? 64 : (a.k_n <= 128 ? 128 : 256);
+  const int n_tiles = (a.k_n + bn - 1) / bn;
+  // largest MT (power of two <= 4) that still gives >= one tile per SM
+  int mt_max = 4;
+  while (mt_max > 1 && ((a.Mp + mt_max * 128 - 1) / (mt_max * 128)) * n_tiles < sms) mt_max /= 2;
+  if (bn == 64) {
+    if (split) {
+      CGB_SW_TRY(2, 64, true, 1, 4)
+      CGB_SW_TRY(1, 64, true, 1, 4)
+    } else {
+      CGB_SW_TRY(4, 64, false, 2, 6)
+      CGB_SW_TRY(2, 64, false, 2, 6)
+      CGB_SW_TRY(1, 64, false, 2, 6)
+    }
+  } else if (bn == 128) {
+    if (split) {
+      CGB_SW_TRY(2, 128, true, 1, 3)
+      CGB_SW_TRY(1, 128, true, 1, 3)
+    } else {
+      CGB_SW_TRY(2, 128, false, 2, 4)
+      CGB_SW_TRY(1, 128, false, 2, 4)
+      CGB_SW_TRY(1, 128, false, 1, 4)
+    }
+  } else {
+    if (split) {
+      CGB_SW_TRY(1, 256, true, 1, 2)
+    } else {
+      CGB_SW_TRY(2, 256, false, 2, 3)
+      CGB_SW_TRY(1, 256, false, 2, 3)
+      CGB_SW_TRY(1, 256, false, 2, 2)
+      CGB_SW_TRY(1, 256, false, 1, 3)
+    }
+  }
+#undef CGB_SW_TRY
+  return cudaErrorNotSupported;
+}
+}  // namespace sw
 
 cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t ldf, const float* I, float* O,
                                    const ConvGeom& g, bool split, cudaStream_t st) {
@@ -366,29 +487,23 @@ cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t
   } else {
     tl = th;
   }
-  const int64_t kn = g.k_n;
-  if (kn <= 64) {
-    if (split) {
-      e = sw::launch_cfg<2, 64, true, 1, 4>(th, tl, I, O, a, st);
-      if (e != cudaErrorNotSupported) return e;
-      return sw::launch_cfg<1, 64, true, 1, 4>(th, tl, I, O, a, st);
-    }
-    e = sw::launch_cfg<4, 64, false, 2, 6>(th, tl, I, O, a, st);
-    if (e != cudaErrorNotSupported) return e;
-    return sw::launch_cfg<2, 64, false, 2, 6>(th, tl, I, O, a, st);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  if (kn <= 128) {
-    if (split) {
-      e = sw::launch_cfg<2, 128, true, 1, 3>(th, tl, I, O, a, st);
-      if (e != cudaErrorNotSupported) return e;
-      return sw::launch_cfg<1, 128, true, 1, 3>(th, tl, I, O, a, st);
-    }
-    e = sw::launch_cfg<2, 128, false, 2, 4>(th, tl, I, O, a, st);
-    if (e != cudaErrorNotSupported) return e;
-    return sw::launch_cfg<1, 128, false, 2, 4>(th, tl, I, O, a, st);
-  }
-  if (split) return sw::launch_cfg<1, 256, true, 1, 2>(th, tl, I, O, a, st);
-  return sw::launch_cfg<1, 256, false, 2, 3>(th, tl, I, O, a, st);
+  return sw::dispatch(th, tl, I, O, a, split, sms, st);
 }
 
 }  // namespace cgb
+
+// Profiling hook (CGB_DEBUG_SW & 64): copies the per-CTA MMA-thread cycle counters
+// of the last shifted-window launch (total, wait t_empty, wait a_full, wait b_full, tiles).
+extern "C" int cgb_debug_sw_stats(unsigned long long* host, int n_cta) {
+  if (!cgb::sw::g_stats) return -1;
+  return cudaMemcpy(host, cgb::sw::g_stats, (size_t)n_cta * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}

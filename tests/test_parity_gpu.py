@@ -218,16 +218,21 @@ def test_kernels_actually_launch():
 
 # ---------------------------------------------------------------- kernel-variant coverage
 VARIANT_CASES = [
-    # (cp, expected path in {shifted, gather}) -- stride-1 windows and the tap-major gather
+    # (cp, expected kernel) -- shifted window (stride 1 and polyphase stride 2) and the gather
     (dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=30, w_i=30, b=2, s=1, p=1), "tcgen05-shifted"),
     (dict(k_n=128, k_h=3, k_w=3, c_i=32, h_i=40, w_i=40, b=3, s=1, p=0), "tcgen05-shifted"),
     (dict(k_n=96, k_h=3, k_w=1, c_i=64, h_i=33, w_i=21, b=2, s=1, p=1), "tcgen05-shifted"),
     (dict(k_n=32, k_h=1, k_w=1, c_i=48, h_i=20, w_i=20, b=3, s=1, p=0), "tcgen05-shifted"),
     (dict(k_n=64, k_h=3, k_w=3, c_i=40, h_i=28, w_i=28, b=1, s=1, p=1), "tcgen05-shifted"),
     (dict(k_n=256, k_h=3, k_w=3, c_i=64, h_i=24, w_i=24, b=2, s=1, p=1), "tcgen05-shifted"),
-    (dict(k_n=512, k_h=3, k_w=3, c_i=64, h_i=7, w_i=7, b=3, s=1, p=1), "tcgen05-gather"),
-    (dict(k_n=96, k_h=3, k_w=3, c_i=48, h_i=15, w_i=15, b=2, s=2, p=1), "tcgen05-gather"),
+    (dict(k_n=512, k_h=3, k_w=3, c_i=64, h_i=7, w_i=7, b=3, s=1, p=1), "tcgen05-shifted"),
+    (dict(k_n=96, k_h=3, k_w=3, c_i=48, h_i=15, w_i=15, b=2, s=2, p=1), "tcgen05-shifted"),
+    (dict(k_n=128, k_h=3, k_w=3, c_i=32, h_i=30, w_i=30, b=2, s=2, p=1), "tcgen05-shifted"),
+    (dict(k_n=64, k_h=1, k_w=1, c_i=64, h_i=28, w_i=28, b=2, s=2, p=0), "tcgen05-shifted"),
+    (dict(k_n=48, k_h=2, k_w=2, c_i=24, h_i=17, w_i=17, b=2, s=2, p=0), "tcgen05-shifted"),
+    (dict(k_n=256, k_h=3, k_w=3, c_i=96, h_i=28, w_i=28, b=1, s=2, p=1), "tcgen05-shifted"),
     (dict(k_n=128, k_h=5, k_w=5, c_i=32, h_i=12, w_i=12, b=2, s=1, p=2), "tcgen05-gather"),
+    (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=20, w_i=20, b=2, s=3, p=1), "tcgen05-gather"),
 ]
 
 
@@ -238,6 +243,9 @@ def test_kernel_variants(orc, case, prec):
     F, I = rand_inputs(cp, 100 + case)
     ref = orc.conv_gemm(F, I, cp)
     O = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo="fused", precision=prec))
-    assert cg.last_path() == path, (cp, cg.last_path())
+    if prec == "tf32":
+        assert cg.last_path() == path, (cp, cg.last_path())
+    else:  # 3xTF32 needs twice the staging; wide polyphase windows fall back to the gather kernel
+        assert cg.last_path() in (path, "tcgen05-gather"), (cp, cg.last_path())
     err = per_output_error(O, ref, orc.output_scale(F, I, cp))
     assert err <= TOL[prec], (cp, prec, err)

@@ -1,4 +1,7 @@
-"""Run one BASELINE layer through the fused operator a few times (for ncu / quick timing)."""
+"""Run one BASELINE layer through the fused operator (for ncu / quick timing).
+
+Timing: `reps` launches enqueued back-to-back between two CUDA events (host launch
+overhead hidden behind device execution), after `warm` warm-up launches."""
 import argparse, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -9,19 +12,44 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--layer", default="r50_3x3_56_64")
 ap.add_argument("--precision", default="tf32")
 ap.add_argument("--algo", default="fused")
-ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--warm", type=int, default=2)
 ap.add_argument("--batch", type=int, default=128)
 a = ap.parse_args()
 layer = [l for l in bench.LAYERS if l[0] == a.layer][0]
 (layer, cp, F, I, O), = bench.make_layer_tensors(cg, torch, [layer], a.batch, 0, 1)
 st = torch.cuda.current_stream()
-ts = []
-for r in range(a.reps):
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
+for _ in range(a.warm):
     cg.conv(F, I, cp, algo=a.algo, precision=a.precision, out=O)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(st)
+for r in range(a.reps):
+    cg.conv(F, I, cp, algo=a.algo, precision=a.precision, out=O)
+e1.record(st)
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.reps
+fl = bench.flops(cp)
+if int(os.environ.get("CGB_DEBUG_SW", "0")) & 64:
+    import numpy as np
+    buf = np.zeros((148, 8), dtype=np.uint64)
+    cg.lib.cgb_debug_sw_stats(buf.ctypes.data, 148)
+    tot, wt, wa, wb, nt = [buf[:, i].astype(np.float64) for i in range(5)]
+    print(f"  MMA thread cycles: total max {tot.max():.0f} mean {tot.mean():.0f}; wait t_empty {wt.mean():.0f} "
+          f"a_full {wa.mean():.0f} b_full {wb.mean():.0f}; tiles max {nt.max():.0f} min {nt.min():.0f}")
+print(f"{a.layer} {a.precision} {cg.last_path()} {ms*1e3:.1f} us  {fl / ms / 1e9:.1f} TFLOPS")
+
+if os.environ.get("CGB_CLOCKS"):
+    # sustained run (~2 s) with nvidia-smi clock sampling
+    cs = bench.ClockSampler(torch.cuda.current_device())
+    cs.start()
+    import time
+    n = max(1, int(2.0 / (ms * 1e-3)))
+    e0.record(st)
+    for r in range(n):
+        cg.conv(F, I, cp, algo=a.algo, precision=a.precision, out=O)
     e1.record(st)
     torch.cuda.synchronize()
-    ts.append(e0.elapsed_time(e1))
-fl = bench.flops(cp)
-print(a.layer, a.precision, cg.last_path(), "ms", ["%.4f" % t for t in ts], "TFLOPS %.1f" % (fl / min(ts) / 1e9))
+    clk = cs.stop()
+    ms2 = e0.elapsed_time(e1) / n
+    print(f"  sustained {n} launches: {ms2*1e3:.1f} us  {fl / ms2 / 1e9:.1f} TFLOPS  clocks {clk}")
