@@ -243,8 +243,8 @@ def make_layer_tensors(cg, torch, layers, b, rank, world, seed=20177):
         gf = torch.Generator(device="cuda").manual_seed(seed + hash(layer[0]) % 1000)
         F.copy_(torch.rand(F.shape, generator=gf, device="cuda") * 2 - 1)
         if world > 1:
-            import torch.distributed as dist
-            dist.broadcast(F, src=0)  # filters broadcast once, outside the timed region
+            from paper_2005_06410_b200.shard import broadcast_filters
+            broadcast_filters(F, src=0)  # filters broadcast once, outside the timed region
         I = cg.empty_tensor4(cp["h_i"], cp["w_i"], cp["c_i"], b)
         I.copy_(torch.rand(I.shape, generator=g, device="cuda") * 2 - 1)
         O = cg.empty_tensor4(cp["k_n"], h_o, w_o, b)
@@ -319,9 +319,10 @@ def run_gpu_arm(args, world, rank, local):
     import paper_2005_06410_b200 as cg
     torch.cuda.set_device(local)
     pk = peaks()
+    from paper_2005_06410_b200.shard import split_range as shard_split
     b = BATCH  # weak scaling: b=128 per GPU (each rank an independent batch shard)
     if args.scaling == "strong":
-        lo, hi = split_range(BATCH, rank, world)
+        lo, hi = shard_split(BATCH, rank, world)  # threads.hpp:20-25 split of the global batch
         b = hi - lo
     tensors = make_layer_tensors(cg, torch, LAYERS, b, rank, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -409,7 +410,7 @@ def run_gpu_arm(args, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="tf32", choices=["tf32", "3xtf32", "auto"])
