@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libconvgemm_b200.so")
+LIB_PATH = os.environ.get("CGB_LIB_OVERRIDE") or os.path.join(HERE, "libconvgemm_b200.so")  # override: profiling
 
 # exported symbols, in include/convgemm_b200.h order
 SYMBOLS = (

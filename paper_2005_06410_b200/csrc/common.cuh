@@ -62,6 +62,10 @@ CGB_DEV void st_global_v8(float* p, const uint32_t* r) {
                : "memory");
 }
 
+CGB_DEV void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 // ------------------------------------------------------------------ mbarrier
 CGB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -85,6 +89,18 @@ CGB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "CGB_WAIT:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra CGB_WAIT;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Spin on mbarrier.test_wait (never suspends the thread): for the single MMA-issuing
+// thread, whose wake-up latency after a suspended try_wait leaves the tensor pipe idle.
+CGB_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "CGB_SPIN:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra CGB_SPIN;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
 }

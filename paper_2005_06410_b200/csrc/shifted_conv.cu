@@ -31,11 +31,14 @@ namespace cgb {
 namespace sw {
 
 constexpr int BK = 32;
-constexpr int PRODUCER_WARPS = 8;
-constexpr int TMA_WARP = 8;
-constexpr int MMA_WARP = 9;
-constexpr int EPI_WARP0 = 10;
-constexpr int THREADS = 14 * 32;
+#ifndef CGB_SW_PWARPS
+#define CGB_SW_PWARPS 8
+#endif
+constexpr int PRODUCER_WARPS = CGB_SW_PWARPS;
+constexpr int TMA_WARP = PRODUCER_WARPS;
+constexpr int MMA_WARP = PRODUCER_WARPS + 1;
+constexpr int EPI_WARP0 = PRODUCER_WARPS + 2;  // 4 consecutive warps cover the 4 TMEM lane quadrants
+constexpr int THREADS = (PRODUCER_WARPS + 6) * 32;
 
 struct Args {
   int32_t k_n, k_h, k_w, c_i, h_i, w_i, p, h_o, w_o, b;
@@ -85,6 +88,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* t_full = b_empty + B_STAGES;
   uint64_t* t_empty = t_full + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2);
+  uint32_t* tap_shift = tmem_holder + 1;  // [taps], filled by the MMA warp
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -118,13 +122,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp < PRODUCER_WARPS) {
     // ---------------------------------------------------------------- window producers
-    // warp w stages row blocks rb = w, w+8, ...: lane = row within the block (32
-    // consecutive padded pixels -> coalesced reads per channel), 32 channels per row.
-    const int row_blocks = (a.R + 31) / 32;
+    // A unit = 32/nph_h consecutive padded rows of each of the nph_h h-phases of one
+    // w-phase: lane l stages row j(l) = l%8 + 8*(l/(8*nph_h)) of h-phase a(l) = (l/8)%nph_h.
+    // For stride 2 the 32 lanes of a warp then read 32 consecutive input rows h (both
+    // parities) -> one 128-byte line per channel; every 8-lane group stores 8 consecutive
+    // rows of one phase -> conflict-free 16-byte shared stores under the 128B swizzle.
+    const int rows_per_unit = 32 / a.nph_h;
+    const int row_blocks = (a.R + rows_per_unit - 1) / rows_per_unit;
+    const int units = a.nph_w * row_blocks;
     const int32_t hw_q = a.Hq * a.Wq;
     const int32_t plane = (int32_t)a.plane;
+    const int lane_row = (lane & 7) + 8 * (lane / (8 * a.nph_h));
+    const int lane_pha = (lane >> 3) % a.nph_h;
+    const uint32_t slot_stride = (uint32_t)a.R_pad * 128;
     int it = 0;  // chunk counter across tiles (slot ring position)
-    // one row block = 32 consecutive padded pixels (lane = row) x 32 channels
     auto row_src = [&](int32_t row, int32_t ph_a, int32_t ph_c, int32_t m0, int cc, bool& ok) -> const float* {
       const int32_t Q = m0 + row;
       ok = row < a.R && Q < a.Mp32;
@@ -145,22 +156,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < BK; ++c) v[c] = (ok && c < cmax) ? __ldg(src + c * plane) : 0.0f;
       }
     };
-    auto store_rows = [&](int32_t row, const float (&v)[BK], uint8_t* dst_hi, uint8_t* dst_lo) {
+    auto store_rows = [&](int32_t row, const float (&v)[BK], uint32_t dst_hi, uint32_t dst_lo) {
       if (row >= a.R) return;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const uint32_t off = row * 128 + ((ch ^ (row & 7)) << 4);
         if (SPLIT) {
-          float4 hi, lo;
-          hi.x = tf32_trunc(v[4 * ch + 0]); lo.x = v[4 * ch + 0] - hi.x;
-          hi.y = tf32_trunc(v[4 * ch + 1]); lo.y = v[4 * ch + 1] - hi.y;
-          hi.z = tf32_trunc(v[4 * ch + 2]); lo.z = v[4 * ch + 2] - hi.z;
-          hi.w = tf32_trunc(v[4 * ch + 3]); lo.w = v[4 * ch + 3] - hi.w;
-          *reinterpret_cast<float4*>(dst_hi + off) = hi;
-          *reinterpret_cast<float4*>(dst_lo + off) = lo;
+          const float h0 = tf32_trunc(v[4 * ch + 0]), h1 = tf32_trunc(v[4 * ch + 1]);
+          const float h2 = tf32_trunc(v[4 * ch + 2]), h3 = tf32_trunc(v[4 * ch + 3]);
+          st_shared_v4(dst_hi + off, h0, h1, h2, h3);
+          st_shared_v4(dst_lo + off, v[4 * ch] - h0, v[4 * ch + 1] - h1, v[4 * ch + 2] - h2, v[4 * ch + 3] - h3);
         } else {
-          *reinterpret_cast<float4*>(dst_hi + off) =
-              make_float4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+          st_shared_v4(dst_hi + off, v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
         }
       }
     };
@@ -170,24 +177,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = it % A_SLOTS;
         const uint32_t ph = (it / A_SLOTS) & 1;
         mbar_wait(&a_empty[s], ph ^ 1);
-        uint8_t* dst_hi = a_slot(s, 0);
-        uint8_t* dst_lo = a_slot(s, SPLIT ? 1 : 0);
+        const uint32_t base_hi = smem_u32(a_slot(s, 0));
+        const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
         const int cmax = a.c_i - cc * BK;
-        // units = (phase, row block); two units in flight per iteration (64 loads per thread)
-        const int units = a.NPH * row_blocks;
+        // two units in flight per iteration (64 loads per thread)
         for (int u = warp; u < units && !(a.dbg & 1); u += 2 * PRODUCER_WARPS) {
           const int u2 = u + PRODUCER_WARPS;
-          const int ph0 = u / row_blocks, rb0 = u - ph0 * row_blocks;
-          const int ph1 = u2 / row_blocks, rb1 = u2 - ph1 * row_blocks;
+          const int pc0 = u / row_blocks, rb0 = u - pc0 * row_blocks;
+          const int pc1 = u2 / row_blocks, rb1 = u2 - pc1 * row_blocks;
+          const int row0 = rb0 * rows_per_unit + lane_row, row1 = rb1 * rows_per_unit + lane_row;
+          const uint32_t off0 = (uint32_t)(lane_pha + a.nph_h * pc0) * slot_stride;
+          const uint32_t off1 = (uint32_t)(lane_pha + a.nph_h * pc1) * slot_stride;
           bool ok0, ok1;
-          const float* s0 = row_src(rb0 * 32 + lane, ph0 % a.nph_h, ph0 / a.nph_h, m0, cc, ok0);
-          const float* s1 = row_src(rb1 * 32 + lane, ph1 % a.nph_h, ph1 / a.nph_h, m0, cc, ok1);
+          const float* s0 = row_src(row0, lane_pha, pc0, m0, cc, ok0);
+          const float* s1 = row_src(row1, lane_pha, pc1, m0, cc, ok1);
           ok1 = ok1 && u2 < units;
           float v0[BK], v1[BK];
           load_rows(s0, ok0, cmax, v0);
           load_rows(s1, ok1, cmax, v1);
-          store_rows(rb0 * 32 + lane, v0, dst_hi + ph0 * a.R_pad * 128, dst_lo + ph0 * a.R_pad * 128);
-          if (u2 < units) store_rows(rb1 * 32 + lane, v1, dst_hi + ph1 * a.R_pad * 128, dst_lo + ph1 * a.R_pad * 128);
+          store_rows(row0, v0, base_hi + off0, base_lo + off0);
+          if (u2 < units) store_rows(row1, v1, base_hi + off1, base_lo + off1);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -198,96 +207,109 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- filter TMA
     if (elect_one()) {
       constexpr uint32_t bytes = C::NS * C::B_TILE;
-      int it = 0;
+      int bs = 0;
+      uint32_t bph = 0;
+      const uint32_t b0_hi = smem_u32(b_slot(0, 0)), b0_lo = smem_u32(b_slot(0, SPLIT ? 1 : 0));
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int n0 = (tile / a.m_tiles) * BN;
         for (int cc = 0; cc < a.CC; ++cc)
-          for (int tap = 0; tap < a.taps; ++tap, ++it) {
-            const int s = it % B_STAGES;
-            const uint32_t ph = (it / B_STAGES) & 1;
-            mbar_wait(&b_empty[s], ph ^ 1);
+          for (int tap = 0; tap < a.taps; ++tap) {
+            mbar_wait_spin(&b_empty[bs], bph ^ 1);
             if (a.dbg & 8) {
-              mbar_arrive(&b_full[s]);
-              continue;
-            }
-            mbar_arrive_expect_tx(&b_full[s], bytes);
+              mbar_arrive(&b_full[bs]);
+            } else {
+              mbar_arrive_expect_tx(&b_full[bs], bytes);
+              const uint32_t stage_off = (uint32_t)bs * C::NS * C::B_TILE;
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j) {
-              tma_load_3d(smem_u32(b_slot(s, 0)) + j * 4096, &tmap_hi, &b_full[s], n0 + 32 * j, tap, cc * BK);
-              if (SPLIT)
-                tma_load_3d(smem_u32(b_slot(s, 1)) + j * 4096, &tmap_lo, &b_full[s], n0 + 32 * j, tap, cc * BK);
+              for (int j = 0; j < BN / 32; ++j) {
+                tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[bs], n0 + 32 * j, tap, cc * BK);
+                if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[bs], n0 + 32 * j, tap, cc * BK);
+              }
             }
+            if (++bs == B_STAGES) { bs = 0; bph ^= 1; }
           }
       }
     }
   } else if (warp == MMA_WARP) {
     // ---------------------------------------------------------------- MMA issue
+    // Per-tap A-descriptor offsets (phase plane + row shift, in 16-byte units) are
+    // tabulated once so the single issuing thread does no integer division: its
+    // scalar work between UMMA batches is exposed as tensor-pipe idle time.
+    for (int t = lane; t < a.taps; t += 32) {
+      const int kh = t % a.k_h, kw = t / a.k_h;
+      const int phase = (kh % a.s) + a.nph_h * (kw % a.s);
+      tap_shift[t] = (uint32_t)((phase * a.R_pad + kh / a.s + a.Hq * (kw / a.s)) * 8);
+    }
+    __syncwarp();
     constexpr uint32_t idesc = idesc_tf32(C::UMMA_N, false, true);
     if (elect_one()) {
       // Descriptors are built once per operand slot; per UMMA only the 14-bit start
       // address field moves (row shift d*128 B = d*8 units, k-step 32 B = 2 units,
       // m-subtile 128 rows = 1024 units, B k-step 1024 B = 64 units, 32-filter block
       // 4096 B = 256 units), so each issue is an add on a uniform register.
-      int ait = 0, bit = 0, t = 0;
+      int as = 0, bs = 0, t = 0;
+      uint32_t aph = 0, bph = 0;
       unsigned long long w_t = 0, w_a = 0, w_b = 0, t_start = clock64();
       const bool st = (a.dbg & 64) != 0;
+      const uint64_t a_desc0 = smem_desc(smem_u32(a_slot(0, 0)), 16, 1024);
+      const uint64_t a_lo_off = SPLIT ? (uint64_t)(a_slot_bytes >> 4) : 0;  // lo window follows hi
+      const uint64_t a_slot_units = (uint64_t)(C::NS * a_slot_bytes) >> 4;
+      const uint64_t b_desc0 = smem_desc(smem_u32(b_slot(0, 0)), 4096, 512, 0, kLayoutSW128_32B);
+      constexpr uint64_t b_lo_off = SPLIT ? (uint64_t)(C::B_TILE >> 4) : 0;
+      constexpr uint64_t b_stage_units = (uint64_t)(C::NS * C::B_TILE) >> 4;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++t) {
         const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
         const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
         unsigned long long c0 = st ? clock64() : 0;
-        mbar_wait(&t_empty[acc_set], acc_ph ^ 1);
+        mbar_wait_spin(&t_empty[acc_set], acc_ph ^ 1);
         if (st) w_t += clock64() - c0;
         tc_fence_after();
         const uint32_t d_base = tmem_base + acc_set * C::ACC_COLS;
-        for (int cc = 0; cc < a.CC; ++cc, ++ait) {
-          const int as = ait % A_SLOTS;
+        for (int cc = 0; cc < a.CC; ++cc) {
           unsigned long long c1 = st ? clock64() : 0;
-          mbar_wait(&a_full[as], (ait / A_SLOTS) & 1);
+          mbar_wait_spin(&a_full[as], aph);
           if (st) w_a += clock64() - c1;
           tc_fence_after();
-          const uint64_t a_hi0 = smem_desc(smem_u32(a_slot(as, 0)), 16, 1024);
-          const uint64_t a_lo0 = smem_desc(smem_u32(a_slot(as, SPLIT ? 1 : 0)), 16, 1024);
-          for (int kw = 0; kw < a.k_w; ++kw)
-            for (int kh = 0; kh < a.k_h; ++kh, ++bit) {
-              const int bs = bit % B_STAGES;
-              unsigned long long c2 = st ? clock64() : 0;
-              mbar_wait(&b_full[bs], (bit / B_STAGES) & 1);
-              if (st) w_b += clock64() - c2;
-              tc_fence_after();
-              // phase (kh % s, kw % s) plane, shifted by kh/s rows + Hq*(kw/s) rows
-              const int phase = (kh % a.s) + a.nph_h * (kw % a.s);
-              const uint64_t shift = (uint64_t)((phase * a.R_pad + kh / a.s + a.Hq * (kw / a.s)) * 8);
-              const uint64_t at = a_hi0 + shift, at_lo = a_lo0 + shift;
-              const uint64_t bt = smem_desc(smem_u32(b_slot(bs, 0)), 4096, 512, 0, kLayoutSW128_32B);
-              const uint64_t bt_lo =
-                  smem_desc(smem_u32(b_slot(bs, SPLIT ? 1 : 0)), 4096, 512, 0, kLayoutSW128_32B);
-              const uint32_t first = (cc == 0 && kw == 0 && kh == 0) ? 0u : 1u;
-              if (!(a.dbg & 2)) {
+          const uint64_t a_hi0 = a_desc0 + (uint64_t)as * a_slot_units;
+          uint32_t shift_next = tap_shift[0];
+          for (int tap = 0; tap < a.taps; ++tap) {
+            const uint64_t shift = shift_next;
+            if (tap + 1 < a.taps) shift_next = tap_shift[tap + 1];
+            unsigned long long c2 = st ? clock64() : 0;
+            mbar_wait_spin(&b_full[bs], bph);
+            if (st) w_b += clock64() - c2;
+            tc_fence_after();
+            const uint64_t at = a_hi0 + shift, at_lo = at + a_lo_off;
+            const uint64_t bt = b_desc0 + (uint64_t)bs * b_stage_units, bt_lo = bt + b_lo_off;
+            const uint32_t first = (cc == 0 && tap == 0) ? 0u : 1u;
+            if (!(a.dbg & 2)) {
 #pragma unroll
-                for (int kk = 0; kk < BK / 8; ++kk)
+              for (int kk = 0; kk < BK / 8; ++kk)
 #pragma unroll
-                  for (int hf = 0; hf < BN / C::UMMA_N; ++hf)
+                for (int hf = 0; hf < BN / C::UMMA_N; ++hf)
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
-                      const uint64_t ad = at + (uint64_t)(mt * 1024 + kk * 2);
-                      const uint64_t bd = bt + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
-                      const uint32_t d = d_base + mt * BN + hf * C::UMMA_N;
-                      const uint32_t acc = kk == 0 ? first : 1u;
-                      if (SPLIT) {
-                        const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024 + kk * 2);
-                        const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
-                        mma_tf32(d, ad_lo, bd, idesc, acc);
-                        mma_tf32(d, ad, bd_lo, idesc, 1);
-                        mma_tf32(d, ad, bd, idesc, 1);
-                      } else {
-                        mma_tf32(d, ad, bd, idesc, acc);
-                      }
+                  for (int mt = 0; mt < MT; ++mt) {
+                    const uint64_t ad = at + (uint64_t)(mt * 1024 + kk * 2);
+                    const uint64_t bd = bt + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
+                    const uint32_t d = d_base + mt * BN + hf * C::UMMA_N;
+                    const uint32_t acc = kk == 0 ? first : 1u;
+                    if (SPLIT) {
+                      const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024 + kk * 2);
+                      const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
+                      mma_tf32(d, ad_lo, bd, idesc, acc);
+                      mma_tf32(d, ad, bd_lo, idesc, 1);
+                      mma_tf32(d, ad, bd, idesc, 1);
+                    } else {
+                      mma_tf32(d, ad, bd, idesc, acc);
                     }
-              }
-              if (a.dbg & 32) mbar_arrive(&b_empty[bs]);
-              else mma_commit(&b_empty[bs]);
+                  }
             }
+            if (a.dbg & 32) mbar_arrive(&b_empty[bs]);
+            else mma_commit(&b_empty[bs]);
+            if (++bs == B_STAGES) { bs = 0; bph ^= 1; }
+          }
           mma_commit(&a_empty[as]);
+          if (++as == A_SLOTS) { as = 0; aph ^= 1; }
         }
         mma_commit(&t_full[acc_set]);
       }
@@ -361,7 +383,7 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   a.R = MT * 128 + a.dmax;
   a.R_pad = (a.R + 7) / 8 * 8;
   const uint32_t a_slot_bytes = (uint32_t)(a.NPH * a.R_pad * 128);
-  const size_t smem = (size_t)A_SLOTS * C::NS * a_slot_bytes + (size_t)B_STAGES * C::NS * C::B_TILE + 1024 + 256;
+  const size_t smem = (size_t)A_SLOTS * C::NS * a_slot_bytes + (size_t)B_STAGES * C::NS * C::B_TILE + 1024 + 512;
   if (smem > 227 * 1024) return cudaErrorNotSupported;
   a.m_tiles = (int32_t)((a.Mp + MT * 128 - 1) / (MT * 128));
   a.n_tiles = (a.k_n + BN - 1) / BN;
@@ -417,7 +439,7 @@ static double padded_waste(const ConvGeom& g) {
 }
 
 bool shifted_supported(const ConvGeom& g) {
-  if (g.s > 2 || g.k_n % 4 != 0 || g.c_i < 16) return false;
+  if (g.s > 2 || g.k_n % 4 != 0 || g.c_i < 16 || g.k_h * g.k_w > 64) return false;
   if (padded_waste(g) > 1.7) return false;
   const int64_t hq = g.h_o + (g.k_h - 1) / g.s, wq = g.w_o + (g.k_w - 1) / g.s;
   const int64_t dmax = (g.k_h - 1) / g.s + hq * ((g.k_w - 1) / g.s);
@@ -426,51 +448,72 @@ bool shifted_supported(const ConvGeom& g) {
 }
 
 namespace sw {
-// Try tile configurations from the largest M tile down; a config is skipped when its
-// shared memory does not fit (launch_cfg -> cudaErrorNotSupported) or when it would
-// leave most SMs idle (fewer tiles than SMs while a smaller M tile exists).
-#define CGB_SW_TRY(MT, BN, SPLIT, AS, BS)                                                   \
-  if (mt_max >= MT) {                                                                       \
-    cudaError_t e_ = launch_cfg<MT, BN, SPLIT, AS, BS>(th, tl, I, O, a, st);               \
-    if (e_ != cudaErrorNotSupported) return e_;                                             \
+// Candidate tile configurations (MT x 128 padded rows, BN filters, 3xTF32, A slots,
+// B stages). A config is skipped when its shared memory does not fit
+// (launch_cfg -> cudaErrorNotSupported).
+struct Cand {
+  int mt, bn, split, as, bs;
+};
+static const Cand kCands[] = {
+    {4, 64, 0, 2, 6},  {2, 64, 0, 2, 6},  {1, 64, 0, 2, 6},  {2, 64, 1, 1, 4},  {1, 64, 1, 1, 4},
+    {2, 128, 0, 2, 4}, {2, 128, 0, 1, 4}, {1, 128, 0, 2, 4}, {1, 128, 0, 1, 4}, {2, 128, 1, 1, 3},
+    {1, 128, 1, 1, 3}, {2, 256, 0, 2, 3}, {2, 256, 0, 1, 3}, {1, 256, 0, 2, 3}, {1, 256, 0, 2, 2},
+    {1, 256, 0, 1, 3}, {1, 256, 1, 1, 2},
+};
+constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
+
+static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
+                               const Args& a, cudaStream_t st) {
+#define CGB_SW_CASE(IDX, MT, BN, SP, AS, BS) \
+  case IDX: return launch_cfg<MT, BN, SP, AS, BS>(th, tl, I, O, a, st);
+  switch (i) {
+    CGB_SW_CASE(0, 4, 64, false, 2, 6)
+    CGB_SW_CASE(1, 2, 64, false, 2, 6)
+    CGB_SW_CASE(2, 1, 64, false, 2, 6)
+    CGB_SW_CASE(3, 2, 64, true, 1, 4)
+    CGB_SW_CASE(4, 1, 64, true, 1, 4)
+    CGB_SW_CASE(5, 2, 128, false, 2, 4)
+    CGB_SW_CASE(6, 2, 128, false, 1, 4)
+    CGB_SW_CASE(7, 1, 128, false, 2, 4)
+    CGB_SW_CASE(8, 1, 128, false, 1, 4)
+    CGB_SW_CASE(9, 2, 128, true, 1, 3)
+    CGB_SW_CASE(10, 1, 128, true, 1, 3)
+    CGB_SW_CASE(11, 2, 256, false, 2, 3)
+    CGB_SW_CASE(12, 2, 256, false, 1, 3)
+    CGB_SW_CASE(13, 1, 256, false, 2, 3)
+    CGB_SW_CASE(14, 1, 256, false, 2, 2)
+    CGB_SW_CASE(15, 1, 256, false, 1, 3)
+    CGB_SW_CASE(16, 1, 256, true, 1, 2)
+    default: return cudaErrorNotSupported;
   }
+#undef CGB_SW_CASE
+}
+
+static int bn_for(int k_n) { return k_n <= 64 ? 64 : (k_n <= 128 ? 128 : 256); }
 
 static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, const Args& a,
                             bool split, int sms, cudaStream_t st) {
-  const int bn = a.k_n <= 64 ? 64 : (a.k_n <= 128 ? 128 : 256);
+  const int bn = bn_for(a.k_n);
   const int n_tiles = (a.k_n + bn - 1) / bn;
-  // largest MT (power of two <= 4) that still gives >= one tile per SM
-  int mt_max = 4;
-  while (mt_max > 1 && ((a.Mp + mt_max * 128 - 1) / (mt_max * 128)) * n_tiles < sms) mt_max /= 2;
-  if (bn == 64) {
-    if (split) {
-      CGB_SW_TRY(2, 64, true, 1, 4)
-      CGB_SW_TRY(1, 64, true, 1, 4)
-    } else {
-      CGB_SW_TRY(4, 64, false, 2, 6)
-      CGB_SW_TRY(2, 64, false, 2, 6)
-      CGB_SW_TRY(1, 64, false, 2, 6)
-    }
-  } else if (bn == 128) {
-    if (split) {
-      CGB_SW_TRY(2, 128, true, 1, 3)
-      CGB_SW_TRY(1, 128, true, 1, 3)
-    } else {
-      CGB_SW_TRY(2, 128, false, 2, 4)
-      CGB_SW_TRY(1, 128, false, 2, 4)
-      CGB_SW_TRY(1, 128, false, 1, 4)
-    }
-  } else {
-    if (split) {
-      CGB_SW_TRY(1, 256, true, 1, 2)
-    } else {
-      CGB_SW_TRY(2, 256, false, 2, 3)
-      CGB_SW_TRY(1, 256, false, 2, 3)
-      CGB_SW_TRY(1, 256, false, 2, 2)
-      CGB_SW_TRY(1, 256, false, 1, 3)
-    }
+  if (const char* f = getenv("CGB_SW_CFG")) {  // profiling override: force one candidate
+    const int i = atoi(f);
+    if (i >= 0 && i < kNumCands && kCands[i].bn == bn && kCands[i].split == (int)split)
+      return launch_cand(i, th, tl, I, O, a, st);
   }
-#undef CGB_SW_TRY
+  // Preference (measured, tools/sweep_cfg.sh): a double-buffered window (A slots = 2) first,
+  // then the largest M tile -- bigger M tiles cut the filter-tile TMA traffic per UMMA
+  // (64/MT B/clk of shared-memory writes) -- as long as at least half the SMs get a tile.
+  int mt_max = 4;
+  while (mt_max > 1 && ((a.Mp + mt_max * 128 - 1) / (mt_max * 128)) * n_tiles * 2 < sms) mt_max /= 2;
+  if (const char* f = getenv("CGB_SW_MT")) mt_max = atoi(f);  // profiling override
+  for (int pass = 0; pass < 2; ++pass)
+    for (int i = 0; i < kNumCands; ++i) {
+      const Cand& c = kCands[i];
+      if (c.bn != bn || c.split != (int)split || c.mt > mt_max) continue;
+      if ((pass == 0) != (c.as == 2)) continue;
+      cudaError_t e = launch_cand(i, th, tl, I, O, a, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
   return cudaErrorNotSupported;
 }
 }  // namespace sw
