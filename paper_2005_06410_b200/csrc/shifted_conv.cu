@@ -323,13 +323,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int sub = warp % 4;  // TMEM lane quadrant this warp may access
     const int32_t hw_q = a.Hq * a.Wq;
     const bool vec = (a.k_n % 8) == 0;
+    unsigned long long epi_wait = 0, epi_busy = 0;
     int t = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++t) {
       const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
       const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
       const int32_t m0 = (tile % a.m_tiles) * (MT * 128);
       const int n0 = (tile / a.m_tiles) * BN;
+      unsigned long long e0 = (a.dbg & 64) ? clock64() : 0;
       mbar_wait_warp(&t_full[acc_set], acc_ph);
+      unsigned long long e1 = (a.dbg & 64) ? clock64() : 0;
+      if (a.dbg & 64) epi_wait += e1 - e0;
       tc_fence_after();
 #pragma unroll 1
       for (int mt = 0; mt < MT && !(a.dbg & 16); ++mt) {
@@ -365,6 +369,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&t_empty[acc_set]);
+      if (a.dbg & 64) epi_busy += clock64() - e1;
+    }
+    if ((a.dbg & 64) && warp == EPI_WARP0 && lane == 0) {
+      a.stats[blockIdx.x * 8 + 5] = epi_wait;
+      a.stats[blockIdx.x * 8 + 6] = epi_busy;
     }
   }
   tc_fence_before();

@@ -34,9 +34,10 @@ if int(os.environ.get("CGB_DEBUG_SW", "0")) & 64:
     import numpy as np
     buf = np.zeros((148, 8), dtype=np.uint64)
     cg.lib.cgb_debug_sw_stats(buf.ctypes.data, 148)
-    tot, wt, wa, wb, nt = [buf[:, i].astype(np.float64) for i in range(5)]
+    tot, wt, wa, wb, nt, ew, eb = [buf[:, i].astype(np.float64) for i in range(7)]
     print(f"  MMA thread cycles: total max {tot.max():.0f} mean {tot.mean():.0f}; wait t_empty {wt.mean():.0f} "
-          f"a_full {wa.mean():.0f} b_full {wb.mean():.0f}; tiles max {nt.max():.0f} min {nt.min():.0f}")
+          f"a_full {wa.mean():.0f} b_full {wb.mean():.0f}; tiles max {nt.max():.0f} min {nt.min():.0f}; "
+          f"epilogue wait {ew.mean():.0f} busy {eb.mean():.0f}")
 print(f"{a.layer} {a.precision} {cg.last_path()} {ms*1e3:.1f} us  {fl / ms / 1e9:.1f} TFLOPS")
 
 if os.environ.get("CGB_CLOCKS"):
