@@ -24,6 +24,7 @@
 // warp 9 MMA issue, warps 10-13 epilogue (TMEM lanes 64*... per warp%4).
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 
 #include "internal.h"
 
@@ -59,21 +60,27 @@ struct Args {
                       //   4 = skip epilogue stores, 8 = skip filter TMA
 };
 
-template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES>
+template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR = false>
 struct Cfg {
   static constexpr int NS = SPLIT ? 2 : 1;
-  static constexpr int B_TILE = BN * BK * 4;
+  static constexpr int NB = PAIR ? BN / 2 : BN;  // filters staged in this CTA (half per CTA for a pair)
+  static constexpr int B_TILE = NB * BK * 4;
   static constexpr int ACC_COLS = MT * BN;  // per accumulator set
   static constexpr int TMEM_COLS = 2 * ACC_COLS <= 512 ? 2 * ACC_COLS : ACC_COLS;
   static constexpr int ACC_SETS = 2 * ACC_COLS <= 512 ? 2 : 1;
   static constexpr int UMMA_N = BN > 256 ? 256 : BN;
 };
 
-template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES>
+// PAIR = true: launched as clusters of 2 CTAs (a TPC); the leader (rank 0) issues
+// tcgen05.mma.cta_group::2 with M = 256 -- A rows 0-127 from the leader's window, 128-255
+// from the peer's window at the same shared-memory offset, B split into two halves of
+// BN/2 filters (one per CTA), accumulators in both CTAs' TMEM. Per SM this halves the
+// filter-tile TMA traffic, the B operand reads and the B staging footprint.
+template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
     sw_conv_kernel(const __grid_constant__ CUtensorMap tmap_hi, const __grid_constant__ CUtensorMap tmap_lo,
                    const float* __restrict__ I, float* __restrict__ O, Args a, uint32_t a_slot_bytes) {
-  using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES>;
+  using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // [A slots: A_SLOTS x NS x a_slot_bytes][B stages: B_STAGES x NS x B_TILE][barriers]
@@ -92,12 +99,19 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  // Tiles: m_tiles x n_tiles units of (MT*128 rows [x2 for a pair], BN filters); a CTA
+  // (or CTA pair) walks them round-robin. For a pair, this CTA owns rows
+  // [m0 + rank*MT*128, +MT*128) of the pair tile and filters [n0 + rank*BN/2, +BN/2) of B.
   const int total_tiles = a.m_tiles * a.n_tiles;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const int tile0 = PAIR ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int tile_step = PAIR ? (int)nclusters_x() : (int)gridDim.x;
+  constexpr int PAIR_ROWS = (PAIR ? 2 : 1) * MT * 128;
 
   if (warp == TMA_WARP) {
     if (lane == 0) {
       for (int s = 0; s < A_SLOTS; ++s) {
-        mbar_init(&a_full[s], PRODUCER_WARPS);
+        mbar_init(&a_full[s], PRODUCER_WARPS * (PAIR ? 2 : 1));
         mbar_init(&a_empty[s], 1);
       }
       for (int s = 0; s < B_STAGES; ++s) {
@@ -106,19 +120,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       for (int s = 0; s < 2; ++s) {
         mbar_init(&t_full[s], 1);
-        mbar_init(&t_empty[s], 4);
+        mbar_init(&t_empty[s], 4 * (PAIR ? 2 : 1));
       }
       fence_mbar_init();
       tma_prefetch_desc(&tmap_hi);
       if (SPLIT) tma_prefetch_desc(&tmap_lo);
     }
     __syncwarp();
-    tmem_alloc(tmem_holder, C::TMEM_COLS);
+  }
+  if (PAIR) cluster_sync();  // peer barriers initialised before any remote arrive
+  if (warp == TMA_WARP) {
+    if (PAIR) tmem_alloc2(tmem_holder, C::TMEM_COLS);
+    else tmem_alloc(tmem_holder, C::TMEM_COLS);
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // cluster addresses of the leader's barriers (arrivals from both CTAs land there)
+  const uint32_t lead_a_full = PAIR ? mapa_shared(a_full, 0) : smem_u32(a_full);
+  const uint32_t lead_b_full = PAIR ? mapa_shared(b_full, 0) : smem_u32(b_full);
+  const uint32_t lead_t_empty = PAIR ? mapa_shared(t_empty, 0) : smem_u32(t_empty);
 
   if (warp < PRODUCER_WARPS) {
     // ---------------------------------------------------------------- window producers
@@ -171,12 +194,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     };
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const int32_t m0 = (tile % a.m_tiles) * (MT * 128);
+    for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+      const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
       for (int cc = 0; cc < a.CC; ++cc, ++it) {
         const int s = it % A_SLOTS;
         const uint32_t ph = (it / A_SLOTS) & 1;
-        mbar_wait(&a_empty[s], ph ^ 1);
+        if (PAIR) mbar_wait_cl(&a_empty[s], ph ^ 1);
+        else mbar_wait(&a_empty[s], ph ^ 1);
         const uint32_t base_hi = smem_u32(a_slot(s, 0));
         const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
         const int cmax = a.c_i - cc * BK;
@@ -200,30 +224,42 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&a_full[s]);
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_cluster(lead_a_full + s * 8);
+          else mbar_arrive(&a_full[s]);
+        }
       }
     }
   } else if (warp == TMA_WARP) {
     // ---------------------------------------------------------------- filter TMA
     if (elect_one()) {
-      constexpr uint32_t bytes = C::NS * C::B_TILE;
+      constexpr uint32_t bytes = C::NS * C::B_TILE * (PAIR ? 2 : 1);  // both halves signal the leader
       int bs = 0;
       uint32_t bph = 0;
       const uint32_t b0_hi = smem_u32(b_slot(0, 0)), b0_lo = smem_u32(b_slot(0, SPLIT ? 1 : 0));
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const int n0 = (tile / a.m_tiles) * BN;
+      for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+        const int n0 = (tile / a.m_tiles) * BN + (int)rank * C::NB;
         for (int cc = 0; cc < a.CC; ++cc)
           for (int tap = 0; tap < a.taps; ++tap) {
-            mbar_wait_spin(&b_empty[bs], bph ^ 1);
+            if (PAIR) mbar_wait_spin_cl(&b_empty[bs], bph ^ 1);
+            else mbar_wait_spin(&b_empty[bs], bph ^ 1);
             if (a.dbg & 8) {
-              mbar_arrive(&b_full[bs]);
+              if (rank == 0) mbar_arrive(&b_full[bs]);
             } else {
-              mbar_arrive_expect_tx(&b_full[bs], bytes);
+              if (rank == 0) mbar_arrive_expect_tx(&b_full[bs], bytes);
               const uint32_t stage_off = (uint32_t)bs * C::NS * C::B_TILE;
 #pragma unroll
-              for (int j = 0; j < BN / 32; ++j) {
-                tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[bs], n0 + 32 * j, tap, cc * BK);
-                if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[bs], n0 + 32 * j, tap, cc * BK);
+              for (int j = 0; j < C::NB / 32; ++j) {
+                if (PAIR) {
+                  tma_load_3d_2sm(b0_hi + stage_off + j * 4096, &tmap_hi, lead_b_full + bs * 8, n0 + 32 * j, tap,
+                                  cc * BK);
+                  if (SPLIT)
+                    tma_load_3d_2sm(b0_lo + stage_off + j * 4096, &tmap_lo, lead_b_full + bs * 8, n0 + 32 * j, tap,
+                                    cc * BK);
+                } else {
+                  tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[bs], n0 + 32 * j, tap, cc * BK);
+                  if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[bs], n0 + 32 * j, tap, cc * BK);
+                }
               }
             }
             if (++bs == B_STAGES) { bs = 0; bph ^= 1; }
@@ -241,8 +277,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       tap_shift[t] = (uint32_t)((phase * a.R_pad + kh / a.s + a.Hq * (kw / a.s)) * 8);
     }
     __syncwarp();
-    constexpr uint32_t idesc = idesc_tf32(C::UMMA_N, false, true);
-    if (elect_one()) {
+    constexpr uint32_t idesc = idesc_tf32(C::UMMA_N, false, true, PAIR ? 256 : 128);
+    if (rank == 0 && elect_one()) {
       // Descriptors are built once per operand slot; per UMMA only the 14-bit start
       // address field moves (row shift d*128 B = d*8 units, k-step 32 B = 2 units,
       // m-subtile 128 rows = 1024 units, B k-step 1024 B = 64 units, 32-filter block
@@ -257,17 +293,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t b_desc0 = smem_desc(smem_u32(b_slot(0, 0)), 4096, 512, 0, kLayoutSW128_32B);
       constexpr uint64_t b_lo_off = SPLIT ? (uint64_t)(C::B_TILE >> 4) : 0;
       constexpr uint64_t b_stage_units = (uint64_t)(C::NS * C::B_TILE) >> 4;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++t) {
+      for (int tile = tile0; tile < total_tiles; tile += tile_step, ++t) {
         const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
         const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
         unsigned long long c0 = st ? clock64() : 0;
-        mbar_wait_spin(&t_empty[acc_set], acc_ph ^ 1);
+        if (PAIR) mbar_wait_spin_cl(&t_empty[acc_set], acc_ph ^ 1);
+        else mbar_wait_spin(&t_empty[acc_set], acc_ph ^ 1);
         if (st) w_t += clock64() - c0;
         tc_fence_after();
         const uint32_t d_base = tmem_base + acc_set * C::ACC_COLS;
         for (int cc = 0; cc < a.CC; ++cc) {
           unsigned long long c1 = st ? clock64() : 0;
-          mbar_wait_spin(&a_full[as], aph);
+          if (PAIR) mbar_wait_spin_cl(&a_full[as], aph);
+          else mbar_wait_spin(&a_full[as], aph);
           if (st) w_a += clock64() - c1;
           tc_fence_after();
           const uint64_t a_hi0 = a_desc0 + (uint64_t)as * a_slot_units;
@@ -276,7 +314,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t shift = shift_next;
             if (tap + 1 < a.taps) shift_next = tap_shift[tap + 1];
             unsigned long long c2 = st ? clock64() : 0;
-            mbar_wait_spin(&b_full[bs], bph);
+            if (PAIR) mbar_wait_spin_cl(&b_full[bs], bph);
+            else mbar_wait_spin(&b_full[bs], bph);
             if (st) w_b += clock64() - c2;
             tc_fence_after();
             const uint64_t at = a_hi0 + shift, at_lo = at + a_lo_off;
@@ -296,22 +335,32 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (SPLIT) {
                       const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024 + kk * 2);
                       const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
-                      mma_tf32(d, ad_lo, bd, idesc, acc);
-                      mma_tf32(d, ad, bd_lo, idesc, 1);
-                      mma_tf32(d, ad, bd, idesc, 1);
+                      if (PAIR) {
+                        mma_tf32_2cta(d, ad_lo, bd, idesc, acc);
+                        mma_tf32_2cta(d, ad, bd_lo, idesc, 1);
+                        mma_tf32_2cta(d, ad, bd, idesc, 1);
+                      } else {
+                        mma_tf32(d, ad_lo, bd, idesc, acc);
+                        mma_tf32(d, ad, bd_lo, idesc, 1);
+                        mma_tf32(d, ad, bd, idesc, 1);
+                      }
                     } else {
-                      mma_tf32(d, ad, bd, idesc, acc);
+                      if (PAIR) mma_tf32_2cta(d, ad, bd, idesc, acc);
+                      else mma_tf32(d, ad, bd, idesc, acc);
                     }
                   }
             }
-            if (a.dbg & 32) mbar_arrive(&b_empty[bs]);
+            if (PAIR) mma_commit_mc2(&b_empty[bs], 3);
+            else if (a.dbg & 32) mbar_arrive(&b_empty[bs]);
             else mma_commit(&b_empty[bs]);
             if (++bs == B_STAGES) { bs = 0; bph ^= 1; }
           }
-          mma_commit(&a_empty[as]);
+          if (PAIR) mma_commit_mc2(&a_empty[as], 3);
+          else mma_commit(&a_empty[as]);
           if (++as == A_SLOTS) { as = 0; aph ^= 1; }
         }
-        mma_commit(&t_full[acc_set]);
+        if (PAIR) mma_commit_mc2(&t_full[acc_set], 3);
+        else mma_commit(&t_full[acc_set]);
       }
       if (st) {
         unsigned long long* o = a.stats + blockIdx.x * 8;
@@ -325,13 +374,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool vec = (a.k_n % 8) == 0;
     unsigned long long epi_wait = 0, epi_busy = 0;
     int t = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++t) {
+    for (int tile = tile0; tile < total_tiles; tile += tile_step, ++t) {
       const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
       const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
-      const int32_t m0 = (tile % a.m_tiles) * (MT * 128);
+      const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
       const int n0 = (tile / a.m_tiles) * BN;
       unsigned long long e0 = (a.dbg & 64) ? clock64() : 0;
-      mbar_wait_warp(&t_full[acc_set], acc_ph);
+      if (PAIR) {
+        if (lane == 0) mbar_wait_cl(&t_full[acc_set], acc_ph);
+        __syncwarp();
+      } else {
+        mbar_wait_warp(&t_full[acc_set], acc_ph);
+      }
       unsigned long long e1 = (a.dbg & 64) ? clock64() : 0;
       if (a.dbg & 64) epi_wait += e1 - e0;
       tc_fence_after();
@@ -368,7 +422,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[acc_set]);
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cluster(lead_t_empty + acc_set * 8);
+        else mbar_arrive(&t_empty[acc_set]);
+      }
       if (a.dbg & 64) epi_busy += clock64() - e1;
     }
     if ((a.dbg & 64) && warp == EPI_WARP0 && lane == 0) {
@@ -377,33 +434,53 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();  // the leader's MMAs write the peer's TMEM: both must be done
+  else __syncthreads();
   if (warp == TMA_WARP) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if (PAIR) tmem_dealloc2(tmem_base, C::TMEM_COLS);
+    else tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 
-template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES>
+template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR = false>
 cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, Args a,
                        cudaStream_t st) {
-  using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES>;
+  using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
   a.R = MT * 128 + a.dmax;
   a.R_pad = (a.R + 7) / 8 * 8;
   const uint32_t a_slot_bytes = (uint32_t)(a.NPH * a.R_pad * 128);
   const size_t smem = (size_t)A_SLOTS * C::NS * a_slot_bytes + (size_t)B_STAGES * C::NS * C::B_TILE + 1024 + 512;
   if (smem > 227 * 1024) return cudaErrorNotSupported;
-  a.m_tiles = (int32_t)((a.Mp + MT * 128 - 1) / (MT * 128));
+  constexpr int pair_rows = (PAIR ? 2 : 1) * MT * 128;
+  a.m_tiles = (int32_t)((a.Mp + pair_rows - 1) / pair_rows);
   a.n_tiles = (a.k_n + BN - 1) / BN;
-  auto kern = sw_conv_kernel<MT, BN, SPLIT, A_SLOTS, B_STAGES>;
+  auto kern = sw_conv_kernel<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = a.m_tiles * a.n_tiles;
-  kern<<<std::min(tiles, sms), THREADS, smem, st>>>(th, tl, I, O, a, a_slot_bytes);
+  if (!PAIR) {
+    kern<<<std::min(tiles, sms), THREADS, smem, st>>>(th, tl, I, O, a, a_slot_bytes);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * std::min(tiles, sms / 2)));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, th, tl, I, O, a, a_slot_bytes);
+    if (e != cudaSuccess) return e;
+  }
   count_launch();
   return cudaGetLastError();
 }
@@ -461,38 +538,57 @@ namespace sw {
 // B stages). A config is skipped when its shared memory does not fit
 // (launch_cfg -> cudaErrorNotSupported).
 struct Cand {
-  int mt, bn, split, as, bs;
+  int mt, bn, split, as, bs, pair;
 };
 static const Cand kCands[] = {
-    {4, 64, 0, 2, 6},  {2, 64, 0, 2, 6},  {1, 64, 0, 2, 6},  {2, 64, 1, 1, 4},  {1, 64, 1, 1, 4},
-    {2, 128, 0, 2, 4}, {2, 128, 0, 1, 4}, {1, 128, 0, 2, 4}, {1, 128, 0, 1, 4}, {2, 128, 1, 1, 3},
-    {1, 128, 1, 1, 3}, {2, 256, 0, 2, 3}, {2, 256, 0, 1, 3}, {1, 256, 0, 2, 3}, {1, 256, 0, 2, 2},
-    {1, 256, 0, 1, 3}, {1, 256, 1, 1, 2},
+    // CTA pairs (cta_group::2): B halves per CTA -> deeper filter pipelines
+    {4, 64, 0, 2, 8, 1},  {2, 64, 0, 2, 8, 1},  {1, 64, 0, 2, 8, 1},  {2, 64, 1, 1, 6, 1},  {1, 64, 1, 1, 6, 1},
+    {2, 128, 0, 2, 6, 1}, {1, 128, 0, 2, 4, 1}, {1, 128, 0, 2, 3, 1}, {2, 128, 1, 1, 4, 1}, {1, 128, 1, 1, 3, 1},
+    {2, 256, 0, 2, 4, 1}, {1, 256, 0, 2, 3, 1}, {1, 256, 0, 2, 2, 1}, {1, 256, 1, 1, 2, 1},
+    // single CTA
+    {4, 64, 0, 2, 6, 0},  {2, 64, 0, 2, 6, 0},  {1, 64, 0, 2, 6, 0},  {2, 64, 1, 1, 4, 0},  {1, 64, 1, 1, 4, 0},
+    {2, 128, 0, 2, 4, 0}, {2, 128, 0, 1, 4, 0}, {1, 128, 0, 2, 4, 0}, {1, 128, 0, 1, 4, 0}, {2, 128, 1, 1, 3, 0},
+    {1, 128, 1, 1, 3, 0}, {2, 256, 0, 2, 3, 0}, {2, 256, 0, 1, 3, 0}, {1, 256, 0, 2, 3, 0}, {1, 256, 0, 2, 2, 0},
+    {1, 256, 0, 1, 3, 0}, {1, 256, 1, 1, 2, 0},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st) {
-#define CGB_SW_CASE(IDX, MT, BN, SP, AS, BS) \
-  case IDX: return launch_cfg<MT, BN, SP, AS, BS>(th, tl, I, O, a, st);
+#define CGB_SW_CASE(IDX, MT, BN, SP, AS, BS, PR) \
+  case IDX: return launch_cfg<MT, BN, SP, AS, BS, PR>(th, tl, I, O, a, st);
   switch (i) {
-    CGB_SW_CASE(0, 4, 64, false, 2, 6)
-    CGB_SW_CASE(1, 2, 64, false, 2, 6)
-    CGB_SW_CASE(2, 1, 64, false, 2, 6)
-    CGB_SW_CASE(3, 2, 64, true, 1, 4)
-    CGB_SW_CASE(4, 1, 64, true, 1, 4)
-    CGB_SW_CASE(5, 2, 128, false, 2, 4)
-    CGB_SW_CASE(6, 2, 128, false, 1, 4)
-    CGB_SW_CASE(7, 1, 128, false, 2, 4)
-    CGB_SW_CASE(8, 1, 128, false, 1, 4)
-    CGB_SW_CASE(9, 2, 128, true, 1, 3)
-    CGB_SW_CASE(10, 1, 128, true, 1, 3)
-    CGB_SW_CASE(11, 2, 256, false, 2, 3)
-    CGB_SW_CASE(12, 2, 256, false, 1, 3)
-    CGB_SW_CASE(13, 1, 256, false, 2, 3)
-    CGB_SW_CASE(14, 1, 256, false, 2, 2)
-    CGB_SW_CASE(15, 1, 256, false, 1, 3)
-    CGB_SW_CASE(16, 1, 256, true, 1, 2)
+    CGB_SW_CASE(0, 4, 64, false, 2, 8, true)
+    CGB_SW_CASE(1, 2, 64, false, 2, 8, true)
+    CGB_SW_CASE(2, 1, 64, false, 2, 8, true)
+    CGB_SW_CASE(3, 2, 64, true, 1, 6, true)
+    CGB_SW_CASE(4, 1, 64, true, 1, 6, true)
+    CGB_SW_CASE(5, 2, 128, false, 2, 6, true)
+    CGB_SW_CASE(6, 1, 128, false, 2, 4, true)
+    CGB_SW_CASE(7, 1, 128, false, 2, 3, true)
+    CGB_SW_CASE(8, 2, 128, true, 1, 4, true)
+    CGB_SW_CASE(9, 1, 128, true, 1, 3, true)
+    CGB_SW_CASE(10, 2, 256, false, 2, 4, true)
+    CGB_SW_CASE(11, 1, 256, false, 2, 3, true)
+    CGB_SW_CASE(12, 1, 256, false, 2, 2, true)
+    CGB_SW_CASE(13, 1, 256, true, 1, 2, true)
+    CGB_SW_CASE(14, 4, 64, false, 2, 6, false)
+    CGB_SW_CASE(15, 2, 64, false, 2, 6, false)
+    CGB_SW_CASE(16, 1, 64, false, 2, 6, false)
+    CGB_SW_CASE(17, 2, 64, true, 1, 4, false)
+    CGB_SW_CASE(18, 1, 64, true, 1, 4, false)
+    CGB_SW_CASE(19, 2, 128, false, 2, 4, false)
+    CGB_SW_CASE(20, 2, 128, false, 1, 4, false)
+    CGB_SW_CASE(21, 1, 128, false, 2, 4, false)
+    CGB_SW_CASE(22, 1, 128, false, 1, 4, false)
+    CGB_SW_CASE(23, 2, 128, true, 1, 3, false)
+    CGB_SW_CASE(24, 1, 128, true, 1, 3, false)
+    CGB_SW_CASE(25, 2, 256, false, 2, 3, false)
+    CGB_SW_CASE(26, 2, 256, false, 1, 3, false)
+    CGB_SW_CASE(27, 1, 256, false, 2, 3, false)
+    CGB_SW_CASE(28, 1, 256, false, 2, 2, false)
+    CGB_SW_CASE(29, 1, 256, false, 1, 3, false)
+    CGB_SW_CASE(30, 1, 256, true, 1, 2, false)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -509,20 +605,33 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     if (i >= 0 && i < kNumCands && kCands[i].bn == bn && kCands[i].split == (int)split)
       return launch_cand(i, th, tl, I, O, a, st);
   }
-  // Preference (measured, tools/sweep_cfg.sh): a double-buffered window (A slots = 2) first,
-  // then the largest M tile -- bigger M tiles cut the filter-tile TMA traffic per UMMA
-  // (64/MT B/clk of shared-memory writes) -- as long as at least half the SMs get a tile.
-  int mt_max = 4;
-  while (mt_max > 1 && ((a.Mp + mt_max * 128 - 1) / (mt_max * 128)) * n_tiles * 2 < sms) mt_max /= 2;
-  if (const char* f = getenv("CGB_SW_MT")) mt_max = atoi(f);  // profiling override
-  for (int pass = 0; pass < 2; ++pass)
+  // Preference (measured, tools/sweep_cfg.sh): CTA pairs first (CGB_SW_PAIR=0 disables),
+  // then a double-buffered window (A slots = 2), then the largest M tile -- bigger M
+  // tiles cut the filter-tile TMA traffic per UMMA -- as long as at least half the SMs
+  // (pairs: SM pairs) get a tile.
+  const char* pe = getenv("CGB_SW_PAIR");
+  const bool allow_pair = !(pe && atoi(pe) == 0);
+  for (int pass = 0; pass < 3; ++pass) {
+    const int want_pair = pass == 0 ? 1 : 0;
+    if (want_pair && !allow_pair) continue;
+    int mt_max = 4;
+    const int units = want_pair ? 2 : 1;
+    while (mt_max > 1 && ((a.Mp + units * mt_max * 128 - 1) / (units * mt_max * 128)) * n_tiles * 2 * units < sms)
+      mt_max /= 2;
+    if (const char* f = getenv("CGB_SW_MT")) mt_max = atoi(f);  // profiling override
     for (int i = 0; i < kNumCands; ++i) {
       const Cand& c = kCands[i];
-      if (c.bn != bn || c.split != (int)split || c.mt > mt_max) continue;
-      if ((pass == 0) != (c.as == 2)) continue;
+      if (c.bn != bn || c.split != (int)split || c.mt > mt_max || c.pair != want_pair) continue;
+      if (pass < 2 && c.as != 2) continue;
       cudaError_t e = launch_cand(i, th, tl, I, O, a, st);
-      if (e != cudaErrorNotSupported) return e;
+      if (e != cudaErrorNotSupported) {
+        if (getenv("CGB_SW_VERBOSE"))
+          fprintf(stderr, "[cgb] shifted cand %d: MT=%d BN=%d split=%d A=%d B=%d pair=%d\n", i, c.mt, c.bn, c.split,
+                  c.as, c.bs, c.pair);
+        return e;
+      }
     }
+  }
   return cudaErrorNotSupported;
 }
 }  // namespace sw
