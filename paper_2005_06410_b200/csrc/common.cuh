@@ -147,6 +147,21 @@ CGB_DEV void tma_load_3d(uint32_t dst, const void* tmap, uint64_t* bar, int32_t 
       : "memory");
 }
 
+CGB_DEV void tma_load_4d(uint32_t dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1, int32_t c2,
+                         int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+CGB_DEV float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
 // ------------------------------------------------------------------ tcgen05
 CGB_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
