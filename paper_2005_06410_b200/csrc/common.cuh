@@ -66,6 +66,22 @@ CGB_DEV void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
+// Global load variants for the window producers (CGB_LDG_MODE: 0 = ld.global.nc (LDG
+// constant path), 1 = ld.global with L1 no-allocate, 2 = plain ld.global).
+CGB_DEV float ldg_stream(const float* p) {
+#if defined(CGB_LDG_MODE) && CGB_LDG_MODE == 1
+  float v;
+  asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+#elif defined(CGB_LDG_MODE) && CGB_LDG_MODE == 2
+  float v;
+  asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 // ------------------------------------------------------------------ mbarrier
 CGB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -173,10 +173,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     auto load_rows = [&](const float* src, bool ok, int cmax, float (&v)[BK]) {
       if (cmax >= BK) {
 #pragma unroll
-        for (int c = 0; c < BK; ++c) v[c] = ok ? __ldg(src + c * plane) : 0.0f;
+        for (int c = 0; c < BK; ++c) v[c] = ok ? ldg_stream(src + c * plane) : 0.0f;
       } else {
 #pragma unroll
-        for (int c = 0; c < BK; ++c) v[c] = (ok && c < cmax) ? __ldg(src + c * plane) : 0.0f;
+        for (int c = 0; c < BK; ++c) v[c] = (ok && c < cmax) ? ldg_stream(src + c * plane) : 0.0f;
       }
     };
     auto store_rows = [&](int32_t row, const float (&v)[BK], uint32_t dst_hi, uint32_t dst_lo) {
@@ -199,8 +199,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int cc = 0; cc < a.CC; ++cc, ++it) {
         const int s = it % A_SLOTS;
         const uint32_t ph = (it / A_SLOTS) & 1;
-        if (PAIR) mbar_wait_cl(&a_empty[s], ph ^ 1);
-        else mbar_wait(&a_empty[s], ph ^ 1);
+        // WAR on this CTA's own window: completion of the reading UMMAs is all that is
+        // needed, so a CTA-scope wait (a cluster-scope acquire compiles to an L1 flush).
+        mbar_wait(&a_empty[s], ph ^ 1);
         const uint32_t base_hi = smem_u32(a_slot(s, 0));
         const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
         const int cmax = a.c_i - cc * BK;
@@ -241,8 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int n0 = (tile / a.m_tiles) * BN + (int)rank * C::NB;
         for (int cc = 0; cc < a.CC; ++cc)
           for (int tap = 0; tap < a.taps; ++tap) {
-            if (PAIR) mbar_wait_spin_cl(&b_empty[bs], bph ^ 1);
-            else mbar_wait_spin(&b_empty[bs], bph ^ 1);
+            mbar_wait_spin(&b_empty[bs], bph ^ 1);  // WAR on own smem: CTA scope suffices
             if (a.dbg & 8) {
               if (rank == 0) mbar_arrive(&b_full[bs]);
             } else {
@@ -314,8 +314,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t shift = shift_next;
             if (tap + 1 < a.taps) shift_next = tap_shift[tap + 1];
             unsigned long long c2 = st ? clock64() : 0;
-            if (PAIR) mbar_wait_spin_cl(&b_full[bs], bph);
-            else mbar_wait_spin(&b_full[bs], bph);
+            // TMA completion bytes of both halves land on this (leader's) barrier; the
+            // UMMA reads the data through the async proxy, so a CTA-scope wait suffices.
+            mbar_wait_spin(&b_full[bs], bph);
             if (st) w_b += clock64() - c2;
             tc_fence_after();
             const uint64_t at = a_hi0 + shift, at_lo = at + a_lo_off;
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int n0 = (tile / a.m_tiles) * BN;
       unsigned long long e0 = (a.dbg & 64) ? clock64() : 0;
       if (PAIR) {
-        if (lane == 0) mbar_wait_cl(&t_full[acc_set], acc_ph);
+        if (lane == 0) mbar_wait(&t_full[acc_set], acc_ph);
         __syncwarp();
       } else {
         mbar_wait_warp(&t_full[acc_set], acc_ph);
