@@ -384,13 +384,40 @@ cgb_status cgb_conv_host(int algo, int precision, const float* F_host, const flo
   float* dF = reinterpret_cast<float*>(b);
   float* dI = reinterpret_cast<float*>(b + align_up((int64_t)fb, 256));
   float* dO = reinterpret_cast<float*>(b + align_up((int64_t)fb, 256) + align_up((int64_t)ib, 256));
-  cudaError_t e;
-  if ((e = cudaMemcpyAsync(dF, F_host, fb, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D F");
-  if ((e = cudaMemcpyAsync(dI, I_host, ib, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D I");
-  st = cgb_conv(algo, precision, dF, dI, cp, dO, nullptr, 0, stream);
-  if (st) return st;
-  if ((e = cudaMemcpyAsync(O_host, dO, ob, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return cuda_fail(e, "D2H O");
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "sync");
+  // Batch-chunked pipeline (host_pipe.cu): image i of I and of O are contiguous byte
+  // ranges, so chunk [i0, i0+n) is a conv with b = n on offset pointers.
+  struct Ctx {
+    int algo, precision;
+    const float* dF;
+    const float* dI;
+    float* dO;
+    cgb_conv_params cp;
+    size_t in_items, out_items;
+    cgb_status st;
+  } ctx{algo, precision, dF, dI, dO, *cp, ib / 4 / (size_t)g.b, ob / 4 / (size_t)g.b, CGB_OK};
+  HostPipe io;
+  io.extra.push_back({dF, F_host, fb});
+  io.in_host = I_host;
+  io.in_dev = dI;
+  io.in_item = ib / (size_t)g.b;
+  io.out_host = O_host;
+  io.out_dev = dO;
+  io.out_item = ob / (size_t)g.b;
+  io.items = g.b;
+  io.chunk_items = host_chunk_items(io.in_item, io.out_item, g.b);
+  io.ctx = &ctx;
+  io.compute = [](void* p, int64_t i0, int64_t n, cudaStream_t st) -> cudaError_t {
+    Ctx& c = *static_cast<Ctx*>(p);
+    cgb_conv_params q = c.cp;
+    q.b = n;
+    c.st = cgb_conv(c.algo, c.precision, c.dF, c.dI + (size_t)i0 * c.in_items, &q, c.dO + (size_t)i0 * c.out_items,
+                    nullptr, 0, st);
+    return c.st == CGB_OK ? cudaSuccess : cudaErrorUnknown;
+  };
+  std::string where;
+  const cudaError_t e = run_host_pipeline(io, s, &where);
+  if (ctx.st != CGB_OK) return ctx.st;  // cgb_conv already set the message
+  if (e != cudaSuccess) return cuda_fail(e, where.c_str());
   return CGB_OK;
 }
 

@@ -1,0 +1,317 @@
+// host_pipe.cu -- the host-memory runtime behind cgb_conv_host.
+//
+// The reference entry points are synchronous calls on host buffers (conv.hpp:60-91);
+// on B200 the cost of such a call is the PCIe traffic, not the kernel (≈0.6 ms of
+// kernels against ≈15 ms of copies for the BASELINE workload). The batch is the
+// outermost (slowest) dimension of both I (h x w x c x b) and O (k_n x h_o x w_o x b),
+// so each image is one contiguous byte range on both sides; the runtime cuts the batch
+// into chunks and runs
+//
+//     H2D(chunk k+1)  ||  conv(chunk k)  ||  D2H(chunk k-1)
+//
+// on three streams (H2D stream, the caller's compute stream, D2H stream), so the two
+// PCIe directions and the tensor cores all run concurrently and the call costs about
+// max(H2D bytes, D2H bytes) / link bandwidth plus one chunk of fill and drain.
+//
+// Pinned (page-locked) caller buffers are copied directly. Pageable buffers go through
+// a ring of pinned bounce slots; the host-side copies into and out of the ring are
+// split across a small persistent thread pool so they keep up with the link.
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+
+namespace cgb {
+
+// ------------------------------------------------------------------ parallel memcpy pool
+namespace {
+
+// Persistent memcpy pool. A job is up to two (dst, src, n) segments cut into
+// 1 MiB-aligned pieces that the caller and the workers claim with an atomic counter.
+// Workers spin on the job generation for a while before sleeping, so the per-job
+// hand-off costs about a cache-line transfer rather than a futex wake-up.
+class CopyPool {
+ public:
+  struct Seg {
+    void* dst;
+    const void* src;
+    size_t n;
+  };
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  // both segments copied when this returns
+  void copy2(Seg a, Seg b) {
+    const size_t total = a.n + b.n;
+    if (total == 0) return;
+    if (workers_.empty() || total < 2 * kPiece) {
+      if (a.n) std::memcpy(a.dst, a.src, a.n);
+      if (b.n) std::memcpy(b.dst, b.src, b.n);
+      return;
+    }
+    seg_[0] = a;
+    seg_[1] = b;
+    const size_t parts = std::min<size_t>(4 * (workers_.size() + 1), (total + kPiece - 1) / kPiece);
+    per_ = (total + parts - 1) / parts;
+    per_ = (per_ + 4095) & ~size_t(4095);
+    nparts_ = (int)((total + per_ - 1) / per_);
+    pending_.store(nparts_, std::memory_order_relaxed);
+    next_.store(0, std::memory_order_release);  // a straggler claiming from here sees this job
+    gen_.fetch_add(1, std::memory_order_release);  // publishes the job
+    if (sleepers_.load(std::memory_order_acquire) > 0) {
+      std::lock_guard<std::mutex> lk(mu_);
+      cv_.notify_all();
+    }
+    work();
+    while (pending_.load(std::memory_order_acquire) > 0) cpu_relax();
+  }
+
+ private:
+  static constexpr size_t kPiece = size_t(1) << 20;
+  static void cpu_relax() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  CopyPool() {
+    const int hw = (int)std::thread::hardware_concurrency();
+    const char* env = getenv("CGB_HOST_COPY_THREADS");
+    const int n = env ? atoi(env) : std::min(8, std::max(1, hw / 2));
+    for (int i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { run(); });
+  }
+  ~CopyPool() {
+    stop_.store(true);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      cv_.notify_all();
+    }
+    for (auto& t : workers_) t.join();
+  }
+  // claim and copy pieces of the current job until none are left
+  void work() {
+    for (;;) {
+      const int i = next_.fetch_add(1, std::memory_order_acq_rel);
+      if (i >= nparts_) return;
+      size_t lo = (size_t)i * per_, hi = std::min(lo + per_, seg_[0].n + seg_[1].n);
+      for (int k = 0; k < 2 && lo < hi; ++k) {  // the piece may straddle the two segments
+        const Seg& sg = seg_[k];
+        if (lo < sg.n) {
+          const size_t e = std::min(hi, sg.n);
+          std::memcpy(static_cast<char*>(sg.dst) + lo, static_cast<const char*>(sg.src) + lo, e - lo);
+        }
+        lo = lo > sg.n ? lo - sg.n : 0;
+        hi = hi > sg.n ? hi - sg.n : 0;
+      }
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+  void run() {
+    uint64_t seen = gen_.load(std::memory_order_acquire);
+    for (;;) {
+      // spin ~100 us for the next job, then sleep
+      for (int it = 0; it < 20000 && gen_.load(std::memory_order_acquire) == seen && !stop_.load(); ++it)
+        cpu_relax();
+      if (gen_.load(std::memory_order_acquire) == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        sleepers_.fetch_add(1, std::memory_order_acq_rel);
+        cv_.wait(lk, [&] { return stop_.load() || gen_.load(std::memory_order_acquire) != seen; });
+        sleepers_.fetch_sub(1, std::memory_order_acq_rel);
+      }
+      if (stop_.load()) return;
+      seen = gen_.load(std::memory_order_acquire);
+      work();
+    }
+  }
+
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  Seg seg_[2] = {};
+  size_t per_ = 0;
+  int nparts_ = 0;
+  std::atomic<int> next_{0}, pending_{0}, sleepers_{0};
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<bool> stop_{false};
+};
+
+// Per-device pipeline state: the two copy streams, their events, the pinned ring.
+struct DeviceState {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in = nullptr, ev_comp = nullptr, ev_end = nullptr;
+  static constexpr int kSlots = 4;
+  cudaEvent_t ev_slot_in[kSlots] = {}, ev_slot_out[kSlots] = {};
+  char* pin = nullptr;  // [kSlots in][kSlots out] bounce slots
+  size_t slot_bytes = 0;
+  bool ok = false;
+};
+
+std::mutex g_mu;
+std::vector<DeviceState> g_dev;
+
+cudaError_t device_state(int dev, DeviceState** out) {
+  if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
+  DeviceState& d = g_dev[dev];
+  if (!d.ok) {
+    cudaError_t e;
+    const unsigned fl = cudaEventDisableTiming;
+    if ((e = cudaStreamCreateWithFlags(&d.h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&d.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    for (cudaEvent_t* ev : {&d.ev_start, &d.ev_in, &d.ev_comp, &d.ev_end})
+      if ((e = cudaEventCreateWithFlags(ev, fl)) != cudaSuccess) return e;
+    for (int i = 0; i < DeviceState::kSlots; ++i) {
+      if ((e = cudaEventCreateWithFlags(&d.ev_slot_in[i], fl)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&d.ev_slot_out[i], fl)) != cudaSuccess) return e;
+    }
+    d.ok = true;
+  }
+  *out = &d;
+  return cudaSuccess;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+int64_t host_chunk_items(size_t in_item, size_t out_item, int64_t items) {
+  const char* env = getenv("CGB_HOST_CHUNK_MB");
+  const double mb = env ? atof(env) : 8.0;
+  const size_t target = (size_t)std::max(1.0, mb * 1048576.0);
+  const size_t per = std::max<size_t>(1, std::max(in_item, out_item));
+  int64_t c = (int64_t)std::max<size_t>(1, target / per);
+  c = std::max<int64_t>(c, (items + 63) / 64);  // at most 64 chunks
+  return std::min(c, items);
+}
+
+static cudaError_t pipeline(DeviceState* d, const HostPipe& io, cudaStream_t compute, std::string* where) {
+  cudaError_t e = cudaSuccess;
+  const int64_t chunk = io.chunk_items > 0 ? std::min(io.chunk_items, io.items) : io.items;
+  const int64_t nchunks = (io.items + chunk - 1) / chunk;
+  const char* in_h = static_cast<const char*>(io.in_host);
+  char* out_h = static_cast<char*>(io.out_host);
+  char* in_d = static_cast<char*>(io.in_dev);
+  const char* out_d = static_cast<const char*>(io.out_dev);
+  const bool direct_in = is_pinned(io.in_host) || getenv("CGB_HOST_NO_BOUNCE");
+  const bool direct_out = is_pinned(io.out_host) || getenv("CGB_HOST_NO_BOUNCE");
+#define CGB_TRY(call, what)       \
+  do {                            \
+    if ((e = (call)) != cudaSuccess) { \
+      *where = what;              \
+      return e;                   \
+    }                             \
+  } while (0)
+  // pinned bounce ring for pageable buffers
+  if (!direct_in || !direct_out) {
+    const size_t need = (size_t)chunk * std::max(io.in_item, io.out_item);
+    if (d->slot_bytes < need) {
+      if (d->pin) cudaFreeHost(d->pin);
+      d->pin = nullptr;
+      d->slot_bytes = 0;
+      CGB_TRY(cudaHostAlloc(reinterpret_cast<void**>(&d->pin), 2 * DeviceState::kSlots * need,
+                            cudaHostAllocPortable),
+              "pinned bounce ring");
+      d->slot_bytes = need;
+    }
+  }
+  auto slot_in = [&](int j) { return d->pin + (size_t)j * d->slot_bytes; };
+  auto slot_out = [&](int j) { return d->pin + (size_t)(DeviceState::kSlots + j) * d->slot_bytes; };
+  CopyPool& pool = CopyPool::get();
+
+  // The copy streams start after whatever the caller queued on the compute stream.
+  CGB_TRY(cudaEventRecord(d->ev_start, compute), "event record");
+  CGB_TRY(cudaStreamWaitEvent(d->h2d, d->ev_start, 0), "stream wait");
+  CGB_TRY(cudaStreamWaitEvent(d->d2h, d->ev_start, 0), "stream wait");
+  for (const HostPipe::Extra& x : io.extra)  // per-call operands (the filters) go first
+    CGB_TRY(cudaMemcpyAsync(x.dev, x.host, x.bytes, cudaMemcpyDefault, d->h2d), "H2D operand");
+
+  // Pageable buffers: in iteration k the host fills bounce slot k%S with input chunk k
+  // and empties the same slot's output half (chunk k-S) in ONE parallel copy job, then
+  // queues H2D(k), conv(k), D2H(k); the device runs S chunks behind the host.
+  constexpr int S = DeviceState::kSlots;
+  auto out_seg = [&](int64_t k) -> CopyPool::Seg {
+    const int64_t i0 = k * chunk, n = std::min(chunk, io.items - i0);
+    return {out_h + (size_t)i0 * io.out_item, slot_out((int)(k % S)), (size_t)n * io.out_item};
+  };
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int j = (int)(k % S);
+    const int64_t i0 = k * chunk, n = std::min(chunk, io.items - i0);
+    const size_t ib = (size_t)n * io.in_item, ob = (size_t)n * io.out_item;
+    // ---- host side of the bounce ring
+    CopyPool::Seg seg_in{nullptr, nullptr, 0}, seg_out{nullptr, nullptr, 0};
+    if (!direct_in) {
+      if (k >= S) CGB_TRY(cudaEventSynchronize(d->ev_slot_in[j]), "bounce slot wait");
+      seg_in = {slot_in(j), in_h + (size_t)i0 * io.in_item, ib};
+    }
+    if (!direct_out && k >= S) {
+      CGB_TRY(cudaEventSynchronize(d->ev_slot_out[j]), "bounce slot wait");
+      seg_out = out_seg(k - S);
+    }
+    pool.copy2(seg_in, seg_out);
+    // ---- H2D
+    CGB_TRY(cudaMemcpyAsync(in_d + (size_t)i0 * io.in_item, direct_in ? in_h + (size_t)i0 * io.in_item : slot_in(j),
+                            ib, cudaMemcpyDefault, d->h2d),
+            "H2D input");
+    if (!direct_in) CGB_TRY(cudaEventRecord(d->ev_slot_in[j], d->h2d), "event record");
+    CGB_TRY(cudaEventRecord(d->ev_in, d->h2d), "event record");
+    // ---- compute
+    CGB_TRY(cudaStreamWaitEvent(compute, d->ev_in, 0), "stream wait");
+    if ((e = io.compute(io.ctx, i0, n, compute)) != cudaSuccess) {
+      *where = "conv";
+      return e;
+    }
+    CGB_TRY(cudaEventRecord(d->ev_comp, compute), "event record");
+    // ---- D2H
+    CGB_TRY(cudaStreamWaitEvent(d->d2h, d->ev_comp, 0), "stream wait");
+    CGB_TRY(cudaMemcpyAsync(direct_out ? out_h + (size_t)i0 * io.out_item : slot_out(j),
+                            out_d + (size_t)i0 * io.out_item, ob, cudaMemcpyDefault, d->d2h),
+            "D2H output");
+    if (!direct_out) CGB_TRY(cudaEventRecord(d->ev_slot_out[j], d->d2h), "event record");
+  }
+  if (!direct_out)
+    for (int64_t k = std::max<int64_t>(0, nchunks - S); k < nchunks; ++k) {
+      CGB_TRY(cudaEventSynchronize(d->ev_slot_out[k % S]), "D2H output");
+      pool.copy2(out_seg(k), {nullptr, nullptr, 0});
+    }
+  // join: the compute stream ends after the last D2H (the call is synchronous anyway)
+  CGB_TRY(cudaEventRecord(d->ev_end, d->d2h), "event record");
+  CGB_TRY(cudaStreamWaitEvent(compute, d->ev_end, 0), "stream wait");
+  CGB_TRY(cudaEventRecord(d->ev_end, d->h2d), "event record");
+  CGB_TRY(cudaStreamWaitEvent(compute, d->ev_end, 0), "stream wait");
+  CGB_TRY(cudaStreamSynchronize(compute), "sync");
+#undef CGB_TRY
+  return cudaSuccess;
+}
+
+cudaError_t run_host_pipeline(const HostPipe& io, cudaStream_t compute, std::string* where) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  DeviceState* d = nullptr;
+  if (e == cudaSuccess) e = device_state(dev, &d);
+  if (e != cudaSuccess) {
+    *where = "host pipeline setup";
+    return e;
+  }
+  e = pipeline(d, io, compute, where);
+  if (e != cudaSuccess) {  // never return with copies still reading/writing caller memory
+    cudaStreamSynchronize(d->h2d);
+    cudaStreamSynchronize(d->d2h);
+    cudaStreamSynchronize(compute);
+  }
+  return e;
+}
+
+}  // namespace cgb

@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+#include <vector>
+
 #include "common.cuh"
 
 namespace cgb {
@@ -58,5 +61,24 @@ cudaError_t launch_tc_gather(const float* f_hi, const float* f_lo, const float* 
 bool shifted_supported(const ConvGeom& g);
 cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t ldf, const float* I, float* O,
                                    const ConvGeom& g, bool split, cudaStream_t st);
+
+// Host-memory runtime (host_pipe.cu): batch-chunked H2D || compute || D2H over three
+// streams, pinned bounce ring + parallel memcpy for pageable caller buffers.
+struct HostPipe {
+  struct Extra { void* dev; const void* host; size_t bytes; };
+  std::vector<Extra> extra;  // copied H2D once, before the first chunk
+  const void* in_host = nullptr;
+  void* in_dev = nullptr;
+  size_t in_item = 0;  // bytes per batch item (image) of the input
+  void* out_host = nullptr;
+  const void* out_dev = nullptr;
+  size_t out_item = 0;
+  int64_t items = 0, chunk_items = 0;
+  // runs the device work for items [i0, i0+n) on st
+  cudaError_t (*compute)(void* ctx, int64_t i0, int64_t n, cudaStream_t st) = nullptr;
+  void* ctx = nullptr;
+};
+int64_t host_chunk_items(size_t in_item, size_t out_item, int64_t items);
+cudaError_t run_host_pipeline(const HostPipe& io, cudaStream_t compute, std::string* where);
 
 }  // namespace cgb

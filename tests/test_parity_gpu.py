@@ -172,6 +172,41 @@ def test_host_path_matches_device_path():
             assert np.array_equal(host, dev), (algo, prec)
 
 
+def _pinned_fortran(a):
+    """Fortran-ordered numpy view over page-locked memory holding a copy of a."""
+    t = torch.empty(a.size, dtype=torch.float32, pin_memory=True)
+    v = t.numpy()
+    v[:] = np.asfortranarray(a).reshape(-1, order="F")
+    return v.reshape(a.shape, order="F"), t
+
+
+@pytest.mark.parametrize("chunk_mb", ["0.02", "0.07", "1000"])
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("bounce", [True, False])
+def test_host_pipeline_chunking(monkeypatch, chunk_mb, pinned, bounce):
+    """cgb_conv_host cuts the batch into chunks (H2D || conv || D2H on three streams,
+    pinned bounce ring for pageable buffers). Any chunking -- one chunk, more chunks
+    than bounce slots, a ragged last chunk -- gives the device-path result bit for bit."""
+    cp = dict(k_n=32, k_h=3, k_w=3, c_i=16, h_i=21, w_i=19, b=11, s=2, p=1)
+    F, I = rand_inputs(cp, 12)
+    monkeypatch.setenv("CGB_HOST_CHUNK_MB", chunk_mb)  # 0.02 MB -> 1 image per chunk
+    if not bounce:
+        monkeypatch.setenv("CGB_HOST_NO_BOUNCE", "1")
+    keep = []
+    if pinned:
+        F, kf = _pinned_fortran(F)
+        I, ki = _pinned_fortran(I)
+        keep += [kf, ki]
+    for prec in ("3xtf32", "tf32"):
+        dev = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo="fused", precision=prec))
+        host = cg.conv(F, I, cp, algo="fused", precision=prec)
+        assert np.array_equal(host, dev), (chunk_mb, pinned, bounce, prec)
+        if pinned:
+            ho, kt = _pinned_fortran(np.zeros_like(host))
+            cg.conv(F, I, cp, algo="fused", precision=prec, out=ho)
+            assert np.array_equal(ho, dev)
+
+
 def test_reference_named_entry_points(orc):
     cp = cg.ConvParams(k_n=16, k_h=3, k_w=3, c_i=8, h_i=12, w_i=12, b=2, s=1, p=1)
     F, I = rand_inputs(vars(cp), 40)
