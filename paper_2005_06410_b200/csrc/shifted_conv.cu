@@ -23,6 +23,8 @@
 // Roles (448 threads): warps 0-7 A producers, warp 8 filter TMA + TMEM alloc,
 // warp 9 MMA issue, warps 10-13 epilogue (TMEM lanes 64*... per warp%4).
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cstdio>
 
@@ -55,10 +57,46 @@ struct Args {
   int64_t Mp;         // padded output rows Hq*Wq*b
   int32_t Mp32;       // same, 32-bit (shifted_supported guarantees < 2^31 - tile)
   int64_t plane;      // h_i*w_i
+  // Work split (see SegIter): tiles [0, dp_tiles) whole and round-robin over the
+  // `groups` CTAs (pairs: clusters); the channel-chunk units of the remaining tiles
+  // (sk_units = their count x CC) in one contiguous, balanced range per group.
+  int32_t dp_tiles, sk_units, groups;
+  float* partial;     // stream-K partial accumulators [groups][2][ranks][MT*128*BN]
+  int* counters;      // [sk tile][ranks*4 epilogue warps][arrived, written]; zero between launches
   unsigned long long* stats;  // per-CTA cycle counters when dbg & 64 (profiling only)
   int32_t dbg;        // profiling switches (CGB_DEBUG_SW): 1 = producers skip loads, 2 = skip MMAs,
                       //   4 = skip epilogue stores, 8 = skip filter TMA
 };
+
+// Segment sequence of one group: its whole (data-parallel) tiles gid, gid+G, ... below
+// dp_tiles, then the pieces of its stream-K unit range [sk_begin(gid), sk_begin(gid+1))
+// cut at tile boundaries. Every role of the kernel walks the same sequence; the state
+// is just the segment index j (registers are the binding resource of this kernel).
+CGB_DEV int64_t sk_begin(const Args& a, int g) { return (int64_t)g * a.sk_units / a.groups; }
+CGB_DEV bool seg_get(const Args& a, int gid, int j, int& tile, int& cc0, int& cc1) {
+  const int ndp = gid < a.dp_tiles ? (a.dp_tiles - gid + a.groups - 1) / a.groups : 0;
+  if (j < ndp) {
+    tile = gid + j * a.groups;
+    cc0 = 0;
+    cc1 = a.CC;
+    return true;
+  }
+  j -= ndp;
+  const int ub = (int)sk_begin(a, gid), ue = (int)sk_begin(a, gid + 1);
+  const int t0 = ub / a.CC + j;  // stream-K tile index of piece j
+  const int us = j == 0 ? ub : t0 * a.CC;
+  if (us >= ue) return false;
+  tile = a.dp_tiles + t0;
+  cc0 = us - t0 * a.CC;
+  cc1 = min(a.CC, ue - t0 * a.CC);
+  return true;
+}
+// group whose stream-K range holds unit x
+CGB_DEV int sk_group_of(const Args& a, int x) {
+  int c = (int)((int64_t)x * a.groups / a.sk_units);
+  while (c + 1 < a.groups && sk_begin(a, c + 1) <= x) ++c;
+  return c;
+}
 
 template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR = false>
 struct Cfg {
@@ -69,6 +107,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * ACC_COLS <= 512 ? 2 * ACC_COLS : ACC_COLS;
   static constexpr int ACC_SETS = 2 * ACC_COLS <= 512 ? 2 : 1;
   static constexpr int UMMA_N = BN > 256 ? 256 : BN;
+  static_assert(BN % 64 == 0, "epilogue works in 64-column blocks");
 };
 
 // PAIR = true: launched as clusters of 2 CTAs (a TPC); the leader (rank 0) issues
@@ -102,10 +141,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   // Tiles: m_tiles x n_tiles units of (MT*128 rows [x2 for a pair], BN filters); a CTA
   // (or CTA pair) walks them round-robin. For a pair, this CTA owns rows
   // [m0 + rank*MT*128, +MT*128) of the pair tile and filters [n0 + rank*BN/2, +BN/2) of B.
-  const int total_tiles = a.m_tiles * a.n_tiles;
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
-  const int tile0 = PAIR ? (int)cluster_id_x() : (int)blockIdx.x;
-  const int tile_step = PAIR ? (int)nclusters_x() : (int)gridDim.x;
+  const int gid = PAIR ? (int)cluster_id_x() : (int)blockIdx.x;  // work group (CTA or CTA pair)
   constexpr int PAIR_ROWS = (PAIR ? 2 : 1) * MT * 128;
 
   if (warp == TMA_WARP) {
@@ -194,9 +231,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     };
-    for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+    int tile, cc0, cc1;
+    for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
       const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
-      for (int cc = 0; cc < a.CC; ++cc, ++it) {
+      for (int cc = cc0; cc < cc1; ++cc, ++it) {
         const int s = it % A_SLOTS;
         const uint32_t ph = (it / A_SLOTS) & 1;
         // WAR on this CTA's own window: completion of the reading UMMAs is all that is
@@ -238,9 +276,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       int bs = 0;
       uint32_t bph = 0;
       const uint32_t b0_hi = smem_u32(b_slot(0, 0)), b0_lo = smem_u32(b_slot(0, SPLIT ? 1 : 0));
-      for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+      int tile, cc0, cc1;
+      for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
         const int n0 = (tile / a.m_tiles) * BN + (int)rank * C::NB;
-        for (int cc = 0; cc < a.CC; ++cc)
+        for (int cc = cc0; cc < cc1; ++cc)
           for (int tap = 0; tap < a.taps; ++tap) {
             mbar_wait_spin(&b_empty[bs], bph ^ 1);  // WAR on own smem: CTA scope suffices
             if (a.dbg & 8) {
@@ -293,7 +332,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t b_desc0 = smem_desc(smem_u32(b_slot(0, 0)), 4096, 512, 0, kLayoutSW128_32B);
       constexpr uint64_t b_lo_off = SPLIT ? (uint64_t)(C::B_TILE >> 4) : 0;
       constexpr uint64_t b_stage_units = (uint64_t)(C::NS * C::B_TILE) >> 4;
-      for (int tile = tile0; tile < total_tiles; tile += tile_step, ++t) {
+      int tile, cc0, cc1;
+      for (; seg_get(a, gid, t, tile, cc0, cc1); ++t) {
         const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
         const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
         unsigned long long c0 = st ? clock64() : 0;
@@ -302,7 +342,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (st) w_t += clock64() - c0;
         tc_fence_after();
         const uint32_t d_base = tmem_base + acc_set * C::ACC_COLS;
-        for (int cc = 0; cc < a.CC; ++cc) {
+        for (int cc = cc0; cc < cc1; ++cc) {
           unsigned long long c1 = st ? clock64() : 0;
           if (PAIR) mbar_wait_spin_cl(&a_full[as], aph);
           else mbar_wait_spin(&a_full[as], aph);
@@ -321,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             tc_fence_after();
             const uint64_t at = a_hi0 + shift, at_lo = at + a_lo_off;
             const uint64_t bt = b_desc0 + (uint64_t)bs * b_stage_units, bt_lo = bt + b_lo_off;
-            const uint32_t first = (cc == 0 && tap == 0) ? 0u : 1u;
+            const uint32_t first = (cc == cc0 && tap == 0) ? 0u : 1u;
             if (!(a.dbg & 2)) {
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk)
@@ -375,7 +415,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool vec = (a.k_n % 8) == 0;
     unsigned long long epi_wait = 0, epi_busy = 0;
     int t = 0;
-    for (int tile = tile0; tile < total_tiles; tile += tile_step, ++t) {
+    int tile, cc0, cc1;
+    for (; seg_get(a, gid, t, tile, cc0, cc1); ++t) {
       const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
       const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
       const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
@@ -390,6 +431,37 @@ __global__ void __launch_bounds__(THREADS, 1)
       unsigned long long e1 = (a.dbg & 64) ? clock64() : 0;
       if (a.dbg & 64) epi_wait += e1 - e0;
       tc_fence_after();
+      // ---- stream-K piece of a split tile. The host enables stream-K only when every
+      // group's range holds >= CC units, so a split tile has exactly two pieces. Both
+      // arrive once per (CTA rank, epilogue warp); the first parks its partial rows in
+      // the arena, the second adds them to its own (a + b == b + a in fp32, so the
+      // result does not depend on which piece finishes first) and writes O.
+      const bool whole = cc0 == 0 && cc1 == a.CC;
+      int nseg = 1, my_k = 0, c_first = 0, x0 = 0;
+      int* cnt = nullptr;
+      bool last = true;
+      if (!whole) {
+        const int stl = tile - a.dp_tiles;
+        x0 = stl * a.CC;
+        c_first = sk_group_of(a, x0);
+        nseg = 2;
+        my_k = gid - c_first;
+        cnt = a.counters + ((size_t)stl * (PAIR ? 8 : 4) + rank * 4 + sub) * 2;
+        int old = 0;
+        if (lane == 0) old = atomicAdd(cnt, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        last = old == nseg - 1;
+        if (last)
+          while (ld_acquire_gpu(cnt + 1) < nseg - 1) {
+          }
+      }
+      // partial rows of group c's piece of this tile: its first piece (range starts in
+      // this tile) in slot 0, its last piece in slot 1
+      auto slab = [&](int c) -> float* {
+        const int which = sk_begin(a, c) >= x0 ? 0 : 1;
+        return a.partial + ((size_t)(c * 2 + which) * (PAIR ? 2 : 1) + rank) * (size_t)(MT * 128 * BN) +
+               (size_t)lane * 32;
+      };
 #pragma unroll 1
       for (int mt = 0; mt < MT && !(a.dbg & 16); ++mt) {
         const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
@@ -401,24 +473,72 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (hq < a.h_o && wq < a.w_o) P = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
         }
         const uint32_t trow = tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS + mt * BN;
+        if (whole) {
 #pragma unroll 1
-        for (int cb = 0; cb < BN / 64 + (BN % 64 ? 1 : 0); ++cb) {
-          uint32_t r[64];
-          tmem_ld_32x32b_x32(trow + cb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-          if (BN >= 64) tmem_ld_32x32b_x32(trow + cb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-          tmem_ld_wait();
-          const int nb = n0 + cb * 64;
-          if (P >= 0 && !(a.dbg & 4)) {
-            float* dst = O + P * a.k_n + nb;
-            if (vec && nb + 64 <= a.k_n) {
+          for (int cb = 0; cb < BN / 64; ++cb) {
+            uint32_t r[64];
+            tmem_ld_32x32b_x32(trow + cb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            tmem_ld_32x32b_x32(trow + cb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            tmem_ld_wait();
+            const int nb = n0 + cb * 64;
+            if (P >= 0 && !(a.dbg & 4)) {
+              float* dst = O + P * a.k_n + nb;
+              if (vec && nb + 64 <= a.k_n) {
 #pragma unroll
-              for (int j = 0; j < 64; j += 8) st_global_v8(dst + j, &r[j]);
-            } else {
+                for (int j = 0; j < 64; j += 8) st_global_v8(dst + j, &r[j]);
+              } else {
 #pragma unroll
-              for (int j = 0; j < (BN >= 64 ? 64 : 32); ++j)
-                if (nb + j < a.k_n) dst[j] = __uint_as_float(r[j]);
+                for (int j = 0; j < 64; ++j)
+                  if (nb + j < a.k_n) dst[j] = __uint_as_float(r[j]);
+              }
             }
           }
+        } else {
+#pragma unroll 1
+          for (int cb = 0; cb < BN / 32; ++cb) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(trow + cb * 32, r);
+            tmem_ld_wait();
+            const size_t off = (size_t)((mt * 4 + sub) * (BN / 32) + cb) * 1024;
+            if (!last) {
+              float* dst = slab(gid) + off;
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) st_global_cg_v8(dst + j, &r[j]);
+              continue;
+            }
+            {  // own + other: with two pieces the sum is the same whichever arrives last
+              const float* src = slab(c_first + (1 - my_k)) + off;
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                float v[8];
+                ld_global_cg_v8(src + j, v);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) r[j + e] = __float_as_uint(__uint_as_float(r[j + e]) + v[e]);
+              }
+            }
+            const int nb = n0 + cb * 32;
+            if (P >= 0 && !(a.dbg & 4)) {
+              float* dst = O + P * a.k_n + nb;
+              if (vec && nb + 32 <= a.k_n) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) st_global_v8(dst + j, &r[j]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (nb + j < a.k_n) dst[j] = __uint_as_float(r[j]);
+              }
+            }
+          }
+        }
+      }
+      if (!whole) {
+        if (!last) {
+          __threadfence();  // each lane's partial rows before the "written" count
+          __syncwarp();
+          if (lane == 0) atomicAdd(cnt + 1, 1);
+        } else if (lane == 0) {
+          cnt[0] = 0;  // every other piece has arrived and written: reset for the next launch
+          cnt[1] = 0;
         }
       }
       tc_fence_before();
@@ -445,6 +565,58 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ stream-K arena
+// Partial-tile accumulators and arrival counters, one arena per (device, stream) so
+// launches that may run concurrently never share one. The counters are zeroed once at
+// allocation; every launch leaves them zero again (the last arriver resets its pair).
+constexpr double kSkFill = 0.9;  // split when the last round of whole tiles is < 90% full
+struct SkArena {
+  float* partial = nullptr;
+  size_t partial_elems = 0;
+  int* counters = nullptr;
+  size_t ncounters = 0;
+};
+static std::mutex g_sk_mu;
+static std::map<std::pair<int, cudaStream_t>, SkArena> g_sk;
+
+static int sk_env() {
+  const char* e = getenv("CGB_SW_SK");  // 0 = never split, 1 = auto (default), 2 = always
+  return e ? atoi(e) : 1;
+}
+
+static bool sk_arena(cudaStream_t st, size_t partial_elems, size_t ncounters, float** p, int** c) {
+  std::lock_guard<std::mutex> lk(g_sk_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SkArena& ar = g_sk[{dev, st}];
+  if (ar.partial_elems < partial_elems) {
+    if (ar.partial) cudaFree(ar.partial);
+    ar.partial = nullptr;
+    ar.partial_elems = 0;
+    if (cudaMalloc(&ar.partial, partial_elems * sizeof(float)) != cudaSuccess) {
+      cudaGetLastError();
+      ar.partial = nullptr;
+      return false;  // no arena: whole tiles only
+    }
+    ar.partial_elems = partial_elems;
+  }
+  if (ar.ncounters < ncounters) {
+    const size_t n = std::max<size_t>(ncounters, 4096);
+    if (ar.counters) cudaFree(ar.counters);
+    ar.counters = nullptr;
+    ar.ncounters = 0;
+    if (cudaMalloc(&ar.counters, n * sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (cudaMemsetAsync(ar.counters, 0, n * sizeof(int), st) != cudaSuccess) return false;
+    ar.ncounters = n;
+  }
+  *p = ar.partial;
+  *c = ar.counters;
+  return true;
+}
+
 template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR = false>
 cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, Args a,
                        cudaStream_t st) {
@@ -464,11 +636,34 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = a.m_tiles * a.n_tiles;
+  const int gmax = PAIR ? sms / 2 : sms;
+  // Work split: whole tiles round-robin while the last round is well filled; otherwise
+  // the last one-to-two rounds of tiles are split by channel chunk over all groups
+  // (stream-K), which needs the partial-tile arena.
+  a.groups = std::min(tiles, gmax);
+  a.dp_tiles = tiles;
+  a.sk_units = 0;
+  a.partial = nullptr;
+  a.counters = nullptr;
+  const int rounds = (tiles + gmax - 1) / gmax;
+  const double fill = (double)tiles / ((double)rounds * gmax);
+  const int sk_mode = sk_env();
+  // Stream-K needs >= CC units per group (two pieces per split tile): tiles >= groups.
+  if (sk_mode != 0 && a.CC >= 2 && tiles >= gmax && (fill < kSkFill || sk_mode == 2)) {
+    const int dp = std::max(0, tiles / gmax - 1) * gmax;
+    const int sk_tiles = tiles - dp;
+    const size_t slab = (size_t)MT * 128 * BN * (PAIR ? 2 : 1);
+    if (sk_arena(st, (size_t)gmax * 2 * slab, (size_t)sk_tiles * (PAIR ? 8 : 4) * 2, &a.partial, &a.counters)) {
+      a.groups = gmax;
+      a.dp_tiles = dp;
+      a.sk_units = sk_tiles * a.CC;
+    }
+  }
   if (!PAIR) {
-    kern<<<std::min(tiles, sms), THREADS, smem, st>>>(th, tl, I, O, a, a_slot_bytes);
+    kern<<<a.groups, THREADS, smem, st>>>(th, tl, I, O, a, a_slot_bytes);
   } else {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * std::min(tiles, sms / 2)));
+    cfg.gridDim = dim3((unsigned)(2 * a.groups));
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -607,18 +802,32 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
       return launch_cand(i, th, tl, I, O, a, st);
   }
   // Preference (measured, tools/sweep_cfg.sh): CTA pairs first (CGB_SW_PAIR=0 disables),
-  // then a double-buffered window (A slots = 2), then the largest M tile -- bigger M
-  // tiles cut the filter-tile TMA traffic per UMMA -- as long as at least half the SMs
-  // (pairs: SM pairs) get a tile.
+  // then a double-buffered window (A slots = 2), then the M tile the cost model picks.
   const char* pe = getenv("CGB_SW_PAIR");
   const bool allow_pair = !(pe && atoi(pe) == 0);
   for (int pass = 0; pass < 3; ++pass) {
     const int want_pair = pass == 0 ? 1 : 0;
     if (want_pair && !allow_pair) continue;
-    int mt_max = 4;
+    // M tile by a cost model: (rounds of work per group) x (relative time of one tile).
+    // Whole tiles cost ceil(tiles / groups) rounds; with stream-K (tiles >= groups, a
+    // last round < 90% full, >= 2 channel chunks) the work spreads evenly: tiles / groups.
+    // Tile times relative to MT = 2 measured on B200 (bigger M tiles reuse each filter
+    // tile over more rows): MT 1 -> 0.65, 2 -> 1, 4 -> 1.8.
     const int units = want_pair ? 2 : 1;
-    while (mt_max > 1 && ((a.Mp + units * mt_max * 128 - 1) / (units * mt_max * 128)) * n_tiles * 2 * units < sms)
-      mt_max /= 2;
+    const int gmax = want_pair ? sms / 2 : sms;
+    int mt_max = 1;
+    double best = 1e30;
+    for (int mt = 4; mt >= 1; mt /= 2) {
+      const double tt = mt == 4 ? 1.8 : (mt == 2 ? 1.0 : 0.65);
+      const int tiles = (int)((a.Mp + units * mt * 128 - 1) / (units * mt * 128)) * n_tiles;
+      const int rounds = (tiles + gmax - 1) / gmax;
+      const bool sk = sk_env() != 0 && a.CC >= 2 && tiles >= gmax && (double)tiles / (rounds * gmax) < kSkFill;
+      const double cost = (sk ? (double)tiles / gmax * 1.03 : (double)rounds) * tt;
+      if (cost < best * 0.98) {
+        best = cost;
+        mt_max = mt;
+      }
+    }
     if (const char* f = getenv("CGB_SW_MT")) mt_max = atoi(f);  // profiling override
     for (int i = 0; i < kNumCands; ++i) {
       const Cand& c = kCands[i];

@@ -284,3 +284,34 @@ def test_kernel_variants(orc, case, prec):
         assert cg.last_path() in (path, "tcgen05-gather"), (cp, cg.last_path())
     err = per_output_error(O, ref, orc.output_scale(F, I, cp))
     assert err <= TOL[prec], (cp, prec, err)
+
+
+# ---------------------------------------------------------------- stream-K split tiles
+SK_CASES = [
+    # enough M tiles (>= one per SM pair) with a last round < 90% full -> the last
+    # rounds are split by channel chunk across SM pairs, two pieces per split tile
+    dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=28, w_i=28, b=24, s=1, p=1),
+    dict(k_n=128, k_h=3, k_w=3, c_i=64, h_i=56, w_i=56, b=24, s=2, p=1),
+    dict(k_n=96, k_h=3, k_w=3, c_i=80, h_i=20, w_i=20, b=48, s=1, p=1),
+]
+
+
+@pytest.mark.parametrize("case", range(len(SK_CASES)))
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_stream_k(orc, monkeypatch, case, prec):
+    cp = SK_CASES[case]
+    F, I = rand_inputs(cp, 300 + case)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    dF, dI = to_dev(F), to_dev(I)
+    a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    assert cg.last_path() in ("tcgen05-shifted", "tcgen05-gather"), cg.last_path()
+    b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    assert np.array_equal(a, b), "stream-K result must not depend on which piece finishes first"
+    assert per_output_error(a, ref, scale) <= TOL[prec]
+    monkeypatch.setenv("CGB_SW_SK", "0")
+    whole = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    assert per_output_error(whole, ref, scale) <= TOL[prec]
+    if cg.last_path() == "tcgen05-shifted":
+        # the split changes the fp32 summation order of the split tiles: proof it engaged
+        assert not np.array_equal(a, whole)
