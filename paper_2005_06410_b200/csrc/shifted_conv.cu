@@ -35,9 +35,13 @@ namespace sw {
 
 constexpr int BK = 32;
 #ifndef CGB_SW_PWARPS
-#define CGB_SW_PWARPS 8
+#define CGB_SW_PWARPS 12
 #endif
 constexpr int PRODUCER_WARPS = CGB_SW_PWARPS;
+#ifndef CGB_SW_UPI
+#define CGB_SW_UPI 1
+#endif
+constexpr int UPI = CGB_SW_UPI;  // window units each producer warp keeps in flight
 constexpr int TMA_WARP = PRODUCER_WARPS;
 constexpr int MMA_WARP = PRODUCER_WARPS + 1;
 constexpr int EPI_WARP0 = PRODUCER_WARPS + 2;  // 4 consecutive warps cover the 4 TMEM lane quadrants
@@ -243,23 +247,27 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t base_hi = smem_u32(a_slot(s, 0));
         const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
         const int cmax = a.c_i - cc * BK;
-        // two units in flight per iteration (64 loads per thread)
-        for (int u = warp; u < units && !(a.dbg & 1); u += 2 * PRODUCER_WARPS) {
-          const int u2 = u + PRODUCER_WARPS;
-          const int pc0 = u / row_blocks, rb0 = u - pc0 * row_blocks;
-          const int pc1 = u2 / row_blocks, rb1 = u2 - pc1 * row_blocks;
-          const int row0 = rb0 * rows_per_unit + lane_row, row1 = rb1 * rows_per_unit + lane_row;
-          const uint32_t off0 = (uint32_t)(lane_pha + a.nph_h * pc0) * slot_stride;
-          const uint32_t off1 = (uint32_t)(lane_pha + a.nph_h * pc1) * slot_stride;
-          bool ok0, ok1;
-          const float* s0 = row_src(row0, lane_pha, pc0, m0, cc, ok0);
-          const float* s1 = row_src(row1, lane_pha, pc1, m0, cc, ok1);
-          ok1 = ok1 && u2 < units;
-          float v0[BK], v1[BK];
-          load_rows(s0, ok0, cmax, v0);
-          load_rows(s1, ok1, cmax, v1);
-          store_rows(row0, v0, base_hi + off0, base_lo + off0);
-          if (u2 < units) store_rows(row1, v1, base_hi + off1, base_lo + off1);
+        // UPI units in flight per iteration (UPI x 32 loads per thread)
+        for (int u = warp; u < units && !(a.dbg & 1); u += UPI * PRODUCER_WARPS) {
+          float v[UPI][BK];
+          int32_t row[UPI];
+          uint32_t off[UPI];
+          const float* src[UPI];
+          bool ok[UPI];
+#pragma unroll
+          for (int q = 0; q < UPI; ++q) {
+            const int uq = u + q * PRODUCER_WARPS;
+            const int pc = uq / row_blocks, rb = uq - pc * row_blocks;
+            row[q] = rb * rows_per_unit + lane_row;
+            off[q] = (uint32_t)(lane_pha + a.nph_h * pc) * slot_stride;
+            src[q] = row_src(row[q], lane_pha, pc, m0, cc, ok[q]);
+            ok[q] = ok[q] && uq < units;
+          }
+#pragma unroll
+          for (int q = 0; q < UPI; ++q) load_rows(src[q], ok[q], cmax, v[q]);
+#pragma unroll
+          for (int q = 0; q < UPI; ++q)
+            if (q == 0 || u + q * PRODUCER_WARPS < units) store_rows(row[q], v[q], base_hi + off[q], base_lo + off[q]);
         }
         fence_proxy_async_smem();
         __syncwarp();
