@@ -88,53 +88,85 @@ def peaks():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled DURING the timed region: NVML polled every
+    2 ms on a thread (nvidia-smi -lms 100 as a fallback)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self.stop_evt = threading.Event()
+        self.t = None
         self.proc = None
         self.lines = []
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop_evt.is_set():
+            try:
+                self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def start(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
         try:
+            fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t = threading.Thread(target=lambda: self.lines.extend(l.strip() for l in self.proc.stdout),
+                                      daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 7:
-                continue
+        if self.nvml:
+            self.stop_evt.set()
+            self.t.join(timeout=1)
+            src = "nvml 2 ms"
+        elif self.proc:
+            self.proc.terminate()
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for ln in self.lines:
+                parts = [x.strip() for x in ln.split(",")]
+                try:
+                    self.samples.append(float(parts[0]))
+                    self.max_mhz = float(parts[1])
+                except (ValueError, IndexError):
+                    continue
+                for nm, v in zip(names, parts[2:6]):
+                    if v.lower() == "active":
+                        self.reasons.add(nm)
+            src = "nvidia-smi 100 ms"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": src}
 
 
 # ----------------------------------------------------------------------------- distributed
@@ -252,31 +284,63 @@ def make_layer_tensors(cg, torch, layers, b, rank, world, seed=20177):
     return out
 
 
-def time_mode(cg, torch, tensors, precision, steps, warmup, flush, world):
+def time_mode(cg, torch, tensors, precision, steps, warmup, flush, world, clocks=None):
+    """Per-layer breakdown from an eager pass (CUDA events around each launch), then
+    the step time from CUDA-graph replays of the 7 launches (host submission out of
+    the device timeline; consecutive kernels overlap setup via programmatic dependent
+    launch). L2 is flushed before every timed step, outside the events."""
     st = torch.cuda.current_stream()
     nl = len(tensors)
-    for _ in range(warmup):
+
+    def step():
         for layer, cp, F, I, O in tensors:
             cg.conv(F, I, cp, algo="fused", precision=precision, out=O)
+
+    for _ in range(warmup):
+        step()
     torch.cuda.synchronize()
+    # eager per-layer pass
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
           for _ in range(steps)]
-    barrier(world)
-    torch.cuda.synchronize()
-    launches0 = cg.kernel_launch_count()
     for s in range(steps):
-        flush.zero_()  # L2 flush (256 MiB write) between timed steps, outside the events
+        flush.zero_()
         for li, (layer, cp, F, I, O) in enumerate(tensors):
             ev[s][li][0].record(st)
             cg.conv(F, I, cp, algo="fused", precision=precision, out=O)
             ev[s][li][1].record(st)
     torch.cuda.synchronize()
-    barrier(world)
-    launches = cg.kernel_launch_count() - launches0
     per_layer = [[ev[s][li][0].elapsed_time(ev[s][li][1]) for s in range(steps)] for li in range(nl)]
-    step_ms = [sum(per_layer[li][s] for li in range(nl)) for s in range(steps)]
-    return per_layer, step_ms, launches
-
+    # graph of one step
+    side = torch.cuda.Stream()
+    side.wait_stream(st)
+    with torch.cuda.stream(side):
+        step()
+    st.wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    l0 = cg.kernel_launch_count()
+    with torch.cuda.graph(g):
+        step()
+    launches_per_step = cg.kernel_launch_count() - l0
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    for s in range(steps):
+        flush.zero_()  # L2 flush (256 MiB write) between timed steps, outside the events
+        sev[s][0].record(st)
+        g.replay()
+        sev[s][1].record(st)
+    torch.cuda.synchronize()
+    clk = clocks.stop() if clocks else None
+    barrier(world)
+    step_ms = [a.elapsed_time(b) for a, b in sev]
+    del g
+    return per_layer, step_ms, launches_per_step * steps, clk
 
 def time_e2e(cg, torch, tensors, precision, steps, warmup, world):
     """Public host-buffer API (cgb_conv_host via cg.conv on numpy arrays backed by
@@ -332,11 +396,10 @@ def run_gpu_arm(args, world, rank, local):
     headline = args.precision
     order = [headline] + [m for m in ("3xtf32",) if m != headline and not args.quick]
     for prec in order:
-        if clocks and prec == headline:
-            clocks.start()
-        per_layer, step_ms, launches = time_mode(cg, torch, tensors, prec, args.steps, args.warmup, flush, world)
-        if clocks and prec == headline:
-            clk = clocks.stop()
+        per_layer, step_ms, launches, c = time_mode(cg, torch, tensors, prec, args.steps, args.warmup, flush, world,
+                                                    clocks if prec == headline else None)
+        if prec == headline:
+            clk = c
         ms_step = statistics.mean(step_ms)
         ms_step = max_over_ranks(ms_step, world)
         step_flops_local = sum(flops(cp) for _, cp, _, _, _ in tensors)
@@ -353,10 +416,9 @@ def run_gpu_arm(args, world, rank, local):
                            "bound": "tensor" if t_tc >= t_hbm else "hbm",
                            "roofline_frac": round(max(t_tc, t_hbm) / t, 4),
                            "tf32_frac": round(t_tc / t, 4)})
-        kern_s = sum(statistics.mean(per_layer[li]) for li in range(len(tensors))) * 1e-3
         modes[prec] = {"value": total_flops / (ms_step * 1e-3) / 1e9, "ms_per_step": ms_step,
                        "layers": layers, "gpu_launches": launches,
-                       "achieved_tflops": step_flops_local / kern_s / 1e12}
+                       "achieved_tflops": step_flops_local / (ms_step * 1e-3) / 1e12}
     # e2e through the host-buffer public API (headline precision)
     e2e_ms, h2d, d2h = time_e2e(cg, torch, tensors, headline, max(1, min(args.steps, 3)), 1, world)
     e2e_ms = max_over_ranks(e2e_ms, world)
@@ -389,6 +451,8 @@ def run_gpu_arm(args, world, rank, local):
                    "global_batch": BATCH * world if args.scaling == "weak" else BATCH, "batch_per_gpu": b,
                    "layers": [l[0] for l in LAYERS], "precision": headline, "algo": "fused",
                    "l2": "256 MiB L2 flush between timed steps (outside the CUDA events); per-step traffic > L2",
+                   "launch": "one CUDA-graph replay of the 7 layer launches per step (programmatic dependent launch "
+                             "between kernels); per-layer times from an eager pass",
                    "parallelism": f"batch-sharded dp{world}, no collective in the timed region"},
         "roofline": {"bound": "tensor", "achieved": hm["achieved_tflops"], "peak": pk["tf32_tflops"],
                      "unit": "TFLOP/s", "frac": hm["achieved_tflops"] / pk["tf32_tflops"], "traffic": traffic,
@@ -398,7 +462,7 @@ def run_gpu_arm(args, world, rank, local):
         "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "cgb_conv_host (host buffers, pinned)"},
         "gpu_launches": hm["gpu_launches"],
-        "clocks": clk if clocks else None,
+        "clocks": clk,
         "modes": {m: {"value": v["value"], "ms_per_step": v["ms_per_step"],
                       "tf32_frac": v["achieved_tflops"] / pk["tf32_tflops"],
                       "per_layer_tflops": {l["layer"]: l["tflops"] for l in v["layers"]}} for m, v in modes.items()},
@@ -410,7 +474,7 @@ def run_gpu_arm(args, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="tf32", choices=["tf32", "3xtf32", "auto"])

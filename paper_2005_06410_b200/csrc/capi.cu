@@ -25,6 +25,30 @@ namespace cgb {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+cudaError_t capture_safe_malloc(void** p, size_t bytes, bool zero) {
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaSuccess && zero) {
+    static thread_local cudaStream_t side = nullptr;
+    if (!side) e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemsetAsync(*p, 0, bytes, side);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(side);
+  }
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (e != cudaSuccess) cudaGetLastError();
+  return e;
+}
+
+bool can_free_now(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs == cudaStreamCaptureStatusNone;
+}
+
 static thread_local std::string g_last_error;
 static thread_local int g_last_path = 0;
 
@@ -130,7 +154,7 @@ struct Scratch {
 };
 static Scratch g_scratch;
 
-static cgb_status scratch_get(size_t need, void** out) {
+static cgb_status scratch_get(size_t need, void** out, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_scratch.mu);
   int dev = 0;
   cudaGetDevice(&dev);
@@ -145,15 +169,16 @@ static cgb_status scratch_get(size_t need, void** out) {
     return fail(CGB_ALLOCATION_FAILURE, "workspace limit exceeded: " + std::to_string(need) +
                                             " bytes requested, limit " + std::to_string(lim));
   if (g_scratch.ptr) {
-    cudaFree(g_scratch.ptr);  // synchronises: no kernel still reads the old buffer
+    // cudaFree synchronises (no kernel still reads the old buffer); while a graph is
+    // being captured the old buffer is leaked instead (freeing would break the capture)
+    if (can_free_now(st)) cudaFree(g_scratch.ptr);
     g_scratch.current.store(0);
     g_scratch.ptr = nullptr;
     g_scratch.bytes = 0;
   }
   void* p = nullptr;
   const size_t alloc = std::max<size_t>(need, size_t(1) << 20);
-  if (cudaMalloc(&p, alloc) != cudaSuccess) {
-    cudaGetLastError();
+  if (capture_safe_malloc(&p, alloc) != cudaSuccess) {
     return fail(CGB_ALLOCATION_FAILURE, "cannot allocate " + std::to_string(alloc) + " bytes of device workspace");
   }
   g_scratch.ptr = p;
@@ -270,7 +295,7 @@ cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, con
       ws = static_cast<uint8_t*>(workspace);
     } else {
       void* p = nullptr;
-      if ((st = scratch_get(need, &p))) return st;
+      if ((st = scratch_get(need, &p, s))) return st;
       ws = static_cast<uint8_t*>(p);
     }
   }

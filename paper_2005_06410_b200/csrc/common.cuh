@@ -34,6 +34,24 @@ CGB_DEV uint32_t smem_u32(const void* p) {
 
 CGB_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch: wait until the previous grid in the stream has
+// completed and its memory is visible (a no-op when launched without the attribute),
+// and allow the next grid to be scheduled early (its CTAs still wait in their own
+// griddep_wait before touching memory).
+CGB_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+CGB_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+CGB_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+CGB_DEV uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+
 CGB_DEV bool elect_one() {
   uint32_t pred = 0;
   asm volatile(

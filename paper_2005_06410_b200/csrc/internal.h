@@ -15,6 +15,14 @@ namespace cgb {
 // Launch accounting (cgb_kernel_launch_count): every kernel launch site bumps it.
 void count_launch(uint64_t n = 1);
 
+// Device allocation that is legal while a stream is being captured into a CUDA graph
+// (the thread's capture mode is relaxed around cudaMalloc; nothing is enqueued), and
+// zero-filled when zero = true (on a private stream, synchronously).
+cudaError_t capture_safe_malloc(void** p, size_t bytes, bool zero = false);
+// True when the calling thread may free device memory now (no capture in progress on
+// `st`; cudaFree would otherwise invalidate the capture).
+bool can_free_now(cudaStream_t st);
+
 // K1: explicit lowered matrix B (k x n, column-major, ld = ldb >= k), bit-exact
 // with im2col<float> (im2col.hpp:77-120); rows k..ldb-1 zero-filled.
 cudaError_t launch_im2col(const float* I, float* B, int64_t ldb, const ConvGeom& g, cudaStream_t st);

@@ -142,6 +142,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if ((a.dbg & 64) && threadIdx.x == 0) {
+    a.stats[blockIdx.x * 16 + 8] = gtimer();
+    a.stats[blockIdx.x * 16 + 14] = smid();
+  }
   // Tiles: m_tiles x n_tiles units of (MT*128 rows [x2 for a pair], BN filters); a CTA
   // (or CTA pair) walks them round-robin. For a pair, this CTA owns rows
   // [m0 + rank*MT*128, +MT*128) of the pair tile and filters [n0 + rank*BN/2, +BN/2) of B.
@@ -179,6 +183,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // Everything above is private to this CTA (barriers, TMEM, the tensor-map parameter);
+  // global memory is touched only after the previous grid in the stream has finished.
+  griddep_wait();
+  if (threadIdx.x == 0) griddep_launch_dependents();
   // cluster addresses of the leader's barriers (arrivals from both CTAs land there)
   const uint32_t lead_a_full = PAIR ? mapa_shared(a_full, 0) : smem_u32(a_full);
   const uint32_t lead_b_full = PAIR ? mapa_shared(b_full, 0) : smem_u32(b_full);
@@ -277,6 +285,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    if ((a.dbg & 64) && warp == 0 && lane == 0) a.stats[blockIdx.x * 16 + 13] = gtimer();
   } else if (warp == TMA_WARP) {
     // ---------------------------------------------------------------- filter TMA
     if (elect_one()) {
@@ -333,6 +342,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int as = 0, bs = 0, t = 0;
       uint32_t aph = 0, bph = 0;
       unsigned long long w_t = 0, w_a = 0, w_b = 0, t_start = clock64();
+      if (a.dbg & 64) a.stats[blockIdx.x * 16 + 9] = gtimer();
       const bool st = (a.dbg & 64) != 0;
       const uint64_t a_desc0 = smem_desc(smem_u32(a_slot(0, 0)), 16, 1024);
       const uint64_t a_lo_off = SPLIT ? (uint64_t)(a_slot_bytes >> 4) : 0;  // lo window follows hi
@@ -412,8 +422,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         else mma_commit(&t_full[acc_set]);
       }
       if (st) {
-        unsigned long long* o = a.stats + blockIdx.x * 8;
+        unsigned long long* o = a.stats + blockIdx.x * 16;
         o[0] = clock64() - t_start; o[1] = w_t; o[2] = w_a; o[3] = w_b; o[4] = t;
+        o[10] = gtimer();
       }
     }
   } else {
@@ -558,13 +569,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (a.dbg & 64) epi_busy += clock64() - e1;
     }
     if ((a.dbg & 64) && warp == EPI_WARP0 && lane == 0) {
-      a.stats[blockIdx.x * 8 + 5] = epi_wait;
-      a.stats[blockIdx.x * 8 + 6] = epi_busy;
+      a.stats[blockIdx.x * 16 + 5] = epi_wait;
+      a.stats[blockIdx.x * 16 + 6] = epi_busy;
+      a.stats[blockIdx.x * 16 + 11] = gtimer();
     }
   }
   tc_fence_before();
   if (PAIR) cluster_sync();  // the leader's MMAs write the peer's TMEM: both must be done
   else __syncthreads();
+  if ((a.dbg & 64) && threadIdx.x == 0) a.stats[blockIdx.x * 16 + 12] = gtimer();
   if (warp == TMA_WARP) {
     __syncwarp();
     tc_fence_after();
@@ -587,6 +600,14 @@ struct SkArena {
 static std::mutex g_sk_mu;
 static std::map<std::pair<int, cudaStream_t>, SkArena> g_sk;
 
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CGB_PDL");  // 0 = plain stream serialization
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 static int sk_env() {
   const char* e = getenv("CGB_SW_SK");  // 0 = never split, 1 = auto (default), 2 = always
   return e ? atoi(e) : 1;
@@ -598,11 +619,10 @@ static bool sk_arena(cudaStream_t st, size_t partial_elems, size_t ncounters, fl
   cudaGetDevice(&dev);
   SkArena& ar = g_sk[{dev, st}];
   if (ar.partial_elems < partial_elems) {
-    if (ar.partial) cudaFree(ar.partial);
+    if (ar.partial && can_free_now(st)) cudaFree(ar.partial);  // leaked while capturing
     ar.partial = nullptr;
     ar.partial_elems = 0;
-    if (cudaMalloc(&ar.partial, partial_elems * sizeof(float)) != cudaSuccess) {
-      cudaGetLastError();
+    if (capture_safe_malloc(reinterpret_cast<void**>(&ar.partial), partial_elems * sizeof(float)) != cudaSuccess) {
       ar.partial = nullptr;
       return false;  // no arena: whole tiles only
     }
@@ -610,14 +630,11 @@ static bool sk_arena(cudaStream_t st, size_t partial_elems, size_t ncounters, fl
   }
   if (ar.ncounters < ncounters) {
     const size_t n = std::max<size_t>(ncounters, 4096);
-    if (ar.counters) cudaFree(ar.counters);
+    if (ar.counters && can_free_now(st)) cudaFree(ar.counters);
     ar.counters = nullptr;
     ar.ncounters = 0;
-    if (cudaMalloc(&ar.counters, n * sizeof(int)) != cudaSuccess) {
-      cudaGetLastError();
+    if (capture_safe_malloc(reinterpret_cast<void**>(&ar.counters), n * sizeof(int), /*zero=*/true) != cudaSuccess)
       return false;
-    }
-    if (cudaMemsetAsync(ar.counters, 0, n * sizeof(int), st) != cudaSuccess) return false;
     ar.ncounters = n;
   }
   *p = ar.partial;
@@ -667,24 +684,29 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
       a.sk_units = sk_tiles * a.CC;
     }
   }
-  if (!PAIR) {
-    kern<<<a.groups, THREADS, smem, st>>>(th, tl, I, O, a, a_slot_bytes);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * a.groups));
-    cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, th, tl, I, O, a, a_slot_bytes);
-    if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((PAIR ? 2 : 1) * a.groups));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (PAIR) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (pdl_enabled()) {  // overlap this launch's setup with the tail of the previous grid
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  e = cudaLaunchKernelEx(&cfg, kern, th, tl, I, O, a, a_slot_bytes);
+  if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
 }
@@ -713,7 +735,7 @@ static Args make_args(const ConvGeom& g) {
   a.dbg = dbg ? atoi(dbg) : 0;
   a.stats = nullptr;
   if (a.dbg & 64) {
-    if (!g_stats) cudaMalloc(&g_stats, 1024 * 8 * sizeof(unsigned long long));
+    if (!g_stats) capture_safe_malloc(reinterpret_cast<void**>(&g_stats), 1024 * 16 * sizeof(unsigned long long));
     a.stats = g_stats;
   }
   return a;
@@ -877,11 +899,13 @@ cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t
 
 }  // namespace cgb
 
-// Profiling hook (CGB_DEBUG_SW & 64): copies the per-CTA MMA-thread cycle counters
-// of the last shifted-window launch (total, wait t_empty, wait a_full, wait b_full, tiles).
+// Profiling hook (CGB_DEBUG_SW & 64): copies 16 counters per CTA of the last
+// shifted-window launch: MMA-thread cycles (total, wait t_empty, wait a_full, wait
+// b_full), segments, epilogue wait/busy cycles, then %globaltimer stamps (ns): entry,
+// MMA loop start, MMA loop end, epilogue end, exit, producers end; and the SM id.
 extern "C" int cgb_debug_sw_stats(unsigned long long* host, int n_cta) {
   if (!cgb::sw::g_stats) return -1;
-  return cudaMemcpy(host, cgb::sw::g_stats, (size_t)n_cta * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+  return cudaMemcpy(host, cgb::sw::g_stats, (size_t)n_cta * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
                  cudaSuccess
              ? 0
              : -1;

@@ -32,12 +32,23 @@ ms = e0.elapsed_time(e1) / a.reps
 fl = bench.flops(cp)
 if int(os.environ.get("CGB_DEBUG_SW", "0")) & 64:
     import numpy as np
-    buf = np.zeros((148, 8), dtype=np.uint64)
+    buf = np.zeros((148, 16), dtype=np.uint64)
     cg.lib.cgb_debug_sw_stats(buf.ctypes.data, 148)
+    lead = buf[:, 4] > 0  # CTAs whose MMA thread ran (pair leaders)
     tot, wt, wa, wb, nt, ew, eb = [buf[:, i].astype(np.float64) for i in range(7)]
-    print(f"  MMA thread cycles: total max {tot.max():.0f} mean {tot.mean():.0f}; wait t_empty {wt.mean():.0f} "
-          f"a_full {wa.mean():.0f} b_full {wb.mean():.0f}; tiles max {nt.max():.0f} min {nt.min():.0f}; "
-          f"epilogue wait {ew.mean():.0f} busy {eb.mean():.0f}")
+    print(f"  MMA thread cycles (leaders): total max {tot[lead].max():.0f} mean {tot[lead].mean():.0f}; wait t_empty "
+          f"{wt[lead].mean():.0f} a_full {wa[lead].mean():.0f} b_full {wb[lead].mean():.0f}; segments max "
+          f"{nt.max():.0f} min {nt[lead].min():.0f}; epilogue wait {ew.mean():.0f} busy {eb.mean():.0f}")
+    ts = buf[:, 8:14].astype(np.int64)
+    ok = ts[:, 0] > 0
+    t0 = ts[ok, 0].min()
+    rel = (ts[ok] - t0) / 1000.0  # us from the first CTA's entry
+    names = ["entry", "mma_start", "mma_end", "epi_end", "exit", "prod_end"]
+    for i, n in enumerate(names):
+        col = rel[:, i][ts[ok, i] > 0]
+        if len(col):
+            print(f"  {n:9s} us: min {col.min():7.2f} median {np.median(col):7.2f} max {col.max():7.2f}")
+
 print(f"{a.layer} {a.precision} {cg.last_path()} {ms*1e3:.1f} us  {fl / ms / 1e9:.1f} TFLOPS")
 
 if os.environ.get("CGB_CLOCKS"):
