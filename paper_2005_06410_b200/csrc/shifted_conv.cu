@@ -35,17 +35,24 @@ namespace sw {
 
 constexpr int BK = 32;
 #ifndef CGB_SW_PWARPS
-#define CGB_SW_PWARPS 12
+#define CGB_SW_PWARPS 13
 #endif
 constexpr int PRODUCER_WARPS = CGB_SW_PWARPS;
 #ifndef CGB_SW_UPI
 #define CGB_SW_UPI 1
 #endif
 constexpr int UPI = CGB_SW_UPI;  // window units each producer warp keeps in flight
-constexpr int TMA_WARP = PRODUCER_WARPS;
-constexpr int MMA_WARP = PRODUCER_WARPS + 1;
-constexpr int EPI_WARP0 = PRODUCER_WARPS + 2;  // 4 consecutive warps cover the 4 TMEM lane quadrants
-constexpr int THREADS = (PRODUCER_WARPS + 6) * 32;
+#ifndef CGB_SW_SPARE
+#define CGB_SW_SPARE 0
+#endif
+// Warp roles. The sub-partition (warp % 4) of the TMA, MMA-issue and epilogue warps
+// follows the producer count: 13 producers (TMA warp on sub-partition 1, MMA issuer on
+// 2) measured 2-3% faster on B200 than 12 (same-box A/B, tools/cmp_libs.sh); SPARE
+// idle warps are a profiling knob for that placement.
+constexpr int TMA_WARP = PRODUCER_WARPS + CGB_SW_SPARE;
+constexpr int MMA_WARP = TMA_WARP + 1;
+constexpr int EPI_WARP0 = TMA_WARP + 2;  // 4 consecutive warps cover the 4 TMEM lane quadrants
+constexpr int THREADS = (EPI_WARP0 + 4) * 32;
 
 struct Args {
   int32_t k_n, k_h, k_w, c_i, h_i, w_i, p, h_o, w_o, b;
@@ -427,7 +434,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         o[10] = gtimer();
       }
     }
-  } else {
+  } else if (warp >= EPI_WARP0) {
     // ---------------------------------------------------------------- epilogue
     const int sub = warp % 4;  // TMEM lane quadrant this warp may access
     const int32_t hw_q = a.Hq * a.Wq;
@@ -649,12 +656,16 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   a.R = MT * 128 + a.dmax;
   a.R_pad = (a.R + 7) / 8 * 8;
   const uint32_t a_slot_bytes = (uint32_t)(a.NPH * a.R_pad * 128);
-  const size_t smem = (size_t)A_SLOTS * C::NS * a_slot_bytes + (size_t)B_STAGES * C::NS * C::B_TILE + 1024 + 512;
-  if (smem > 227 * 1024) return cudaErrorNotSupported;
+  const size_t base_smem = (size_t)A_SLOTS * C::NS * a_slot_bytes + (size_t)B_STAGES * C::NS * C::B_TILE + 1024 + 1024;
+  if (base_smem > 227 * 1024) return cudaErrorNotSupported;
   constexpr int pair_rows = (PAIR ? 2 : 1) * MT * 128;
   a.m_tiles = (int32_t)((a.Mp + pair_rows - 1) / pair_rows);
   a.n_tiles = (a.k_n + BN - 1) / BN;
+  const size_t smem = base_smem;
   auto kern = sw_conv_kernel<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
+  if (getenv("CGB_SW_VERBOSE"))
+    fprintf(stderr, "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d smem=%.1fKB\n", MT, BN, (int)SPLIT,
+            A_SLOTS, B_STAGES, (int)PAIR, smem / 1024.0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -776,6 +787,8 @@ static const Cand kCands[] = {
     {2, 128, 0, 2, 4, 0}, {2, 128, 0, 1, 4, 0}, {1, 128, 0, 2, 4, 0}, {1, 128, 0, 1, 4, 0}, {2, 128, 1, 1, 3, 0},
     {1, 128, 1, 1, 3, 0}, {2, 256, 0, 2, 3, 0}, {2, 256, 0, 1, 3, 0}, {1, 256, 0, 2, 3, 0}, {1, 256, 0, 2, 2, 0},
     {1, 256, 0, 1, 3, 0}, {1, 256, 1, 1, 2, 0},
+    // CTA pairs with one window slot
+    {2, 64, 0, 1, 8, 1},  {1, 64, 0, 1, 8, 1},  {2, 128, 0, 1, 4, 1}, {1, 128, 0, 1, 4, 1}, {1, 256, 0, 1, 3, 1},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 
@@ -815,6 +828,11 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(28, 1, 256, false, 2, 2, false)
     CGB_SW_CASE(29, 1, 256, false, 1, 3, false)
     CGB_SW_CASE(30, 1, 256, true, 1, 2, false)
+    CGB_SW_CASE(31, 2, 64, false, 1, 8, true)
+    CGB_SW_CASE(32, 1, 64, false, 1, 8, true)
+    CGB_SW_CASE(33, 2, 128, false, 1, 4, true)
+    CGB_SW_CASE(34, 1, 128, false, 1, 4, true)
+    CGB_SW_CASE(35, 1, 256, false, 1, 3, true)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -835,8 +853,9 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
   // then a double-buffered window (A slots = 2), then the M tile the cost model picks.
   const char* pe = getenv("CGB_SW_PAIR");
   const bool allow_pair = !(pe && atoi(pe) == 0);
-  for (int pass = 0; pass < 3; ++pass) {
-    const int want_pair = pass == 0 ? 1 : 0;
+  // passes: pairs with a double-buffered window, pairs with any, single CTAs likewise
+  for (int pass = 0; pass < 4; ++pass) {
+    const int want_pair = pass < 2 ? 1 : 0;
     if (want_pair && !allow_pair) continue;
     // M tile by a cost model: (rounds of work per group) x (relative time of one tile).
     // Whole tiles cost ceil(tiles / groups) rounds; with stream-K (tiles >= groups, a
@@ -862,7 +881,7 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     for (int i = 0; i < kNumCands; ++i) {
       const Cand& c = kCands[i];
       if (c.bn != bn || c.split != (int)split || c.mt > mt_max || c.pair != want_pair) continue;
-      if (pass < 2 && c.as != 2) continue;
+      if (pass % 2 == 0 && c.as != 2) continue;
       cudaError_t e = launch_cand(i, th, tl, I, O, a, st);
       if (e != cudaErrorNotSupported) {
         if (getenv("CGB_SW_VERBOSE"))
