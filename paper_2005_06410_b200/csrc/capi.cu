@@ -129,22 +129,6 @@ cudaError_t make_filter_tmap_tapmajor(CUtensorMap* tm, const float* f, const Con
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t make_input_tmap_runs(CUtensorMap* tm, const float* I, const ConvGeom& g, int box_px, int box_c) {
-  auto enc = get_encode();
-  if (!enc) return cudaErrorNotSupported;
-  const int64_t plane = g.h_i * g.w_i;
-  if ((plane * 4) % 16 != 0 || (box_px * 4) % 16 != 0 || reinterpret_cast<uintptr_t>(I) % 16 != 0)
-    return cudaErrorNotSupported;
-  cuuint64_t dims[3] = {(cuuint64_t)plane, (cuuint64_t)g.c_i, (cuuint64_t)g.b};
-  cuuint64_t strides[2] = {(cuuint64_t)(plane * 4), (cuuint64_t)(g.c_i * plane * 4)};
-  cuuint32_t box[3] = {(cuuint32_t)box_px, (cuuint32_t)box_c, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(I), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
 // ------------------------------------------------------------------ workspace (ScratchTracker)
 struct Scratch {
   std::mutex mu;

@@ -80,17 +80,10 @@ CGB_DEV void st_global_v8(float* p, const uint32_t* r) {
                : "memory");
 }
 
-// Stream-K partial tiles: written and read by different SMs inside one launch, so both
-// sides go through L2 (.cg: no L1 allocation, no stale L1 lines).
-CGB_DEV void st_global_cg_v8(float* p, const uint32_t* r) {
-  asm volatile("st.global.cg.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(r[0]), "r"(r[1]),
-               "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
-}
-CGB_DEV void ld_global_cg_v8(const float* p, float* v) {
-  asm volatile("ld.global.cg.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-               : "l"(p)
+// Stream-K second piece: fire-and-forget vector add into O (REDG.ADD.F32x4, RN).
+CGB_DEV void red_add_v4(float* p, const uint32_t* r) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(r[0])),
+               "f"(__uint_as_float(r[1])), "f"(__uint_as_float(r[2])), "f"(__uint_as_float(r[3]))
                : "memory");
 }
 CGB_DEV int ld_acquire_gpu(const int* p) {

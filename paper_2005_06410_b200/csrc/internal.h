@@ -54,11 +54,6 @@ cudaError_t make_filter_tmap(CUtensorMap* tm, const float* f, int64_t k_n, int64
 // 1 tap x 32 channels, 32-byte-atom 128B swizzle. Needs k_n % 4 == 0.
 cudaError_t make_filter_tmap_tapmajor(CUtensorMap* tm, const float* f, const ConvGeom& g);
 
-// 3-D TMA descriptor over the raw input I seen as (pixel = h + h_i*w, channel, image):
-// box box_px pixels x box_c channels x 1 image, no swizzle, zero fill past the end.
-// Needs (h_i*w_i) % 4 == 0, box_px % 4 == 0 and a 16-byte aligned I.
-cudaError_t make_input_tmap_runs(CUtensorMap* tm, const float* I, const ConvGeom& g, int box_px, int box_c);
-
 // K3 tap-major gather kernel (tc_gather.cu): c_i >= 16, k_n % 4 == 0.
 bool gather_supported(const ConvGeom& g);
 cudaError_t launch_tc_gather(const float* f_hi, const float* f_lo, const float* I, float* O, const ConvGeom& g,

@@ -35,21 +35,20 @@ namespace sw {
 
 constexpr int BK = 32;
 #ifndef CGB_SW_PWARPS
-#define CGB_SW_PWARPS 13
+#define CGB_SW_PWARPS 12
 #endif
 constexpr int PRODUCER_WARPS = CGB_SW_PWARPS;
 #ifndef CGB_SW_UPI
 #define CGB_SW_UPI 1
 #endif
 constexpr int UPI = CGB_SW_UPI;  // window units each producer warp keeps in flight
-#ifndef CGB_SW_SPARE
-#define CGB_SW_SPARE 0
-#endif
-// Warp roles. The sub-partition (warp % 4) of the TMA, MMA-issue and epilogue warps
-// follows the producer count: 13 producers (TMA warp on sub-partition 1, MMA issuer on
-// 2) measured 2-3% faster on B200 than 12 (same-box A/B, tools/cmp_libs.sh); SPARE
-// idle warps are a profiling knob for that placement.
-constexpr int TMA_WARP = PRODUCER_WARPS + CGB_SW_SPARE;
+// Warp roles: producers, the window forwarder (CTA pairs: one thread turns the local
+// "window staged" barrier into one cluster-scope arrive on the leader's barrier per
+// chunk), the filter TMA warp, the MMA issuer, 4 epilogue warps. The sub-partition
+// (warp % 4) of the TMA/MMA/epilogue warps follows from this order; 12 producers plus
+// the forwarder measured best on B200 (same-box A/B, tools/cmp_libs.sh).
+constexpr int FWD_WARP = PRODUCER_WARPS;
+constexpr int TMA_WARP = PRODUCER_WARPS + 1;
 constexpr int MMA_WARP = TMA_WARP + 1;
 constexpr int EPI_WARP0 = TMA_WARP + 2;  // 4 consecutive warps cover the 4 TMEM lane quadrants
 constexpr int THREADS = (EPI_WARP0 + 4) * 32;
@@ -72,8 +71,8 @@ struct Args {
   // `groups` CTAs (pairs: clusters); the channel-chunk units of the remaining tiles
   // (sk_units = their count x CC) in one contiguous, balanced range per group.
   int32_t dp_tiles, sk_units, groups;
-  float* partial;     // stream-K partial accumulators [groups][2][ranks][MT*128*BN]
   int* counters;      // [sk tile][ranks*4 epilogue warps][arrived, written]; zero between launches
+  int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   unsigned long long* stats;  // per-CTA cycle counters when dbg & 64 (profiling only)
   int32_t dbg;        // profiling switches (CGB_DEBUG_SW): 1 = producers skip loads, 2 = skip MMAs,
                       //   4 = skip epilogue stores, 8 = skip filter TMA
@@ -144,7 +143,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* b_empty = b_full + B_STAGES;
   uint64_t* t_full = b_empty + B_STAGES;
   uint64_t* t_empty = t_full + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(t_empty + 2);
+  uint64_t* a_ready = t_empty + 2;  // [A_SLOTS] this CTA's producers done (CTA pairs)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(a_ready + A_SLOTS);
   uint32_t* tap_shift = tmem_holder + 1;  // [taps], filled by the MMA warp
 
   const int warp = threadIdx.x / 32;
@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == TMA_WARP) {
     if (lane == 0) {
       for (int s = 0; s < A_SLOTS; ++s) {
-        mbar_init(&a_full[s], PRODUCER_WARPS * (PAIR ? 2 : 1));
+        mbar_init(&a_full[s], PAIR ? 2 : PRODUCER_WARPS);  // pairs: one forwarded arrive per CTA
+        mbar_init(&a_ready[s], PRODUCER_WARPS);
         mbar_init(&a_empty[s], 1);
       }
       for (int s = 0; s < B_STAGES; ++s) {
@@ -287,12 +288,24 @@ __global__ void __launch_bounds__(THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (PAIR) mbar_arrive_cluster(lead_a_full + s * 8);
-          else mbar_arrive(&a_full[s]);
+          mbar_arrive(PAIR ? &a_ready[s] : &a_full[s]);  // CTA scope: cheap (no GPU-wide fence)
         }
       }
     }
     if ((a.dbg & 64) && warp == 0 && lane == 0) a.stats[blockIdx.x * 16 + 13] = gtimer();
+  } else if (warp == FWD_WARP) {
+    // ---------------------------------------------------------------- window forwarder
+    // A cluster-scope release arrive costs a GPU-wide memory barrier; paying it once per
+    // chunk here keeps it off the producer warps (the bottleneck of staging-bound layers).
+    if (PAIR && lane == 0) {
+      int it = 0, tile, cc0, cc1;
+      for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j)
+        for (int cc = cc0; cc < cc1; ++cc, ++it) {
+          const int s = it % A_SLOTS;
+          mbar_wait(&a_ready[s], (it / A_SLOTS) & 1);
+          mbar_arrive_cluster(lead_a_full + s * 8);
+        }
+    }
   } else if (warp == TMA_WARP) {
     // ---------------------------------------------------------------- filter TMA
     if (elect_one()) {
@@ -438,7 +451,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- epilogue
     const int sub = warp % 4;  // TMEM lane quadrant this warp may access
     const int32_t hw_q = a.Hq * a.Wq;
-    const bool vec = (a.k_n % 8) == 0;
     unsigned long long epi_wait = 0, epi_busy = 0;
     int t = 0;
     int tile, cc0, cc1;
@@ -458,36 +470,25 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (a.dbg & 64) epi_wait += e1 - e0;
       tc_fence_after();
       // ---- stream-K piece of a split tile. The host enables stream-K only when every
-      // group's range holds >= CC units, so a split tile has exactly two pieces. Both
-      // arrive once per (CTA rank, epilogue warp); the first parks its partial rows in
-      // the arena, the second adds them to its own (a + b == b + a in fp32, so the
-      // result does not depend on which piece finishes first) and writes O.
+      // group's range holds >= CC units, so a split tile has exactly two pieces. Each
+      // (CTA rank, epilogue warp) of both pieces arrives once: the first stores its rows
+      // into O like a whole tile and publishes "written"; the second waits for that and
+      // red.adds its rows into O (fire-and-forget, no loads). O = p0 + p1 rounded once,
+      // the same value whichever piece finishes first.
       const bool whole = cc0 == 0 && cc1 == a.CC;
-      int nseg = 1, my_k = 0, c_first = 0, x0 = 0;
       int* cnt = nullptr;
-      bool last = true;
+      bool add = false;
       if (!whole) {
         const int stl = tile - a.dp_tiles;
-        x0 = stl * a.CC;
-        c_first = sk_group_of(a, x0);
-        nseg = 2;
-        my_k = gid - c_first;
         cnt = a.counters + ((size_t)stl * (PAIR ? 8 : 4) + rank * 4 + sub) * 2;
         int old = 0;
         if (lane == 0) old = atomicAdd(cnt, 1);
         old = __shfl_sync(0xffffffffu, old, 0);
-        last = old == nseg - 1;
-        if (last)
-          while (ld_acquire_gpu(cnt + 1) < nseg - 1) {
+        add = old == 1;
+        if (add)
+          while (ld_acquire_gpu(cnt + 1) < 1) {
           }
       }
-      // partial rows of group c's piece of this tile: its first piece (range starts in
-      // this tile) in slot 0, its last piece in slot 1
-      auto slab = [&](int c) -> float* {
-        const int which = sk_begin(a, c) >= x0 ? 0 : 1;
-        return a.partial + ((size_t)(c * 2 + which) * (PAIR ? 2 : 1) + rank) * (size_t)(MT * 128 * BN) +
-               (size_t)lane * 32;
-      };
 #pragma unroll 1
       for (int mt = 0; mt < MT && !(a.dbg & 16); ++mt) {
         const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
@@ -499,71 +500,41 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (hq < a.h_o && wq < a.w_o) P = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
         }
         const uint32_t trow = tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS + mt * BN;
-        if (whole) {
 #pragma unroll 1
-          for (int cb = 0; cb < BN / 64; ++cb) {
-            uint32_t r[64];
-            tmem_ld_32x32b_x32(trow + cb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-            tmem_ld_32x32b_x32(trow + cb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-            tmem_ld_wait();
-            const int nb = n0 + cb * 64;
-            if (P >= 0 && !(a.dbg & 4)) {
-              float* dst = O + P * a.k_n + nb;
-              if (vec && nb + 64 <= a.k_n) {
+        for (int cb = 0; cb < BN / 64; ++cb) {
+          uint32_t r[64];
+          tmem_ld_32x32b_x32(trow + cb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld_32x32b_x32(trow + cb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          tmem_ld_wait();
+          const int nb = n0 + cb * 64;
+          if (P >= 0 && !(a.dbg & 4)) {
+            float* dst = O + P * a.k_n + nb;
+            if (a.vec && nb + 64 <= a.k_n) {
+              if (!add) {
 #pragma unroll
                 for (int j = 0; j < 64; j += 8) st_global_v8(dst + j, &r[j]);
               } else {
 #pragma unroll
-                for (int j = 0; j < 64; ++j)
-                  if (nb + j < a.k_n) dst[j] = __uint_as_float(r[j]);
+                for (int j = 0; j < 64; j += 4) red_add_v4(dst + j, &r[j]);
               }
-            }
-          }
-        } else {
-#pragma unroll 1
-          for (int cb = 0; cb < BN / 32; ++cb) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(trow + cb * 32, r);
-            tmem_ld_wait();
-            const size_t off = (size_t)((mt * 4 + sub) * (BN / 32) + cb) * 1024;
-            if (!last) {
-              float* dst = slab(gid) + off;
+            } else {
 #pragma unroll
-              for (int j = 0; j < 32; j += 8) st_global_cg_v8(dst + j, &r[j]);
-              continue;
-            }
-            {  // own + other: with two pieces the sum is the same whichever arrives last
-              const float* src = slab(c_first + (1 - my_k)) + off;
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                float v[8];
-                ld_global_cg_v8(src + j, v);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) r[j + e] = __float_as_uint(__uint_as_float(r[j + e]) + v[e]);
-              }
-            }
-            const int nb = n0 + cb * 32;
-            if (P >= 0 && !(a.dbg & 4)) {
-              float* dst = O + P * a.k_n + nb;
-              if (vec && nb + 32 <= a.k_n) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 8) st_global_v8(dst + j, &r[j]);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (nb + j < a.k_n) dst[j] = __uint_as_float(r[j]);
-              }
+              for (int j = 0; j < 64; ++j)
+                if (nb + j < a.k_n) {
+                  if (!add) dst[j] = __uint_as_float(r[j]);
+                  else atomicAdd(dst + j, __uint_as_float(r[j]));
+                }
             }
           }
         }
       }
       if (!whole) {
-        if (!last) {
-          __threadfence();  // each lane's partial rows before the "written" count
+        if (!add) {
+          __threadfence();  // each lane's rows before the "written" count
           __syncwarp();
           if (lane == 0) atomicAdd(cnt + 1, 1);
         } else if (lane == 0) {
-          cnt[0] = 0;  // every other piece has arrived and written: reset for the next launch
+          cnt[0] = 0;  // both pieces arrived and the first has written: reset for the next launch
           cnt[1] = 0;
         }
       }
@@ -593,19 +564,17 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-// ------------------------------------------------------------------ stream-K arena
-// Partial-tile accumulators and arrival counters, one arena per (device, stream) so
-// launches that may run concurrently never share one. The counters are zeroed once at
-// allocation; every launch leaves them zero again (the last arriver resets its pair).
+// ------------------------------------------------------------------ stream-K counters
+// Arrival counters of split tiles, one array per (device, stream) so launches that may
+// run concurrently never share one. Zeroed once at allocation; every launch leaves them
+// zero again (the second piece resets its pair).
 constexpr double kSkFill = 0.9;  // split when the last round of whole tiles is < 90% full
-struct SkArena {
-  float* partial = nullptr;
-  size_t partial_elems = 0;
+struct SkCounters {
   int* counters = nullptr;
-  size_t ncounters = 0;
+  size_t n = 0;
 };
 static std::mutex g_sk_mu;
-static std::map<std::pair<int, cudaStream_t>, SkArena> g_sk;
+static std::map<std::pair<int, cudaStream_t>, SkCounters> g_sk;
 
 static bool pdl_enabled() {
   static const bool on = [] {
@@ -620,33 +589,21 @@ static int sk_env() {
   return e ? atoi(e) : 1;
 }
 
-static bool sk_arena(cudaStream_t st, size_t partial_elems, size_t ncounters, float** p, int** c) {
+static int* sk_counters(cudaStream_t st, size_t n) {
   std::lock_guard<std::mutex> lk(g_sk_mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  SkArena& ar = g_sk[{dev, st}];
-  if (ar.partial_elems < partial_elems) {
-    if (ar.partial && can_free_now(st)) cudaFree(ar.partial);  // leaked while capturing
-    ar.partial = nullptr;
-    ar.partial_elems = 0;
-    if (capture_safe_malloc(reinterpret_cast<void**>(&ar.partial), partial_elems * sizeof(float)) != cudaSuccess) {
-      ar.partial = nullptr;
-      return false;  // no arena: whole tiles only
-    }
-    ar.partial_elems = partial_elems;
+  SkCounters& c = g_sk[{dev, st}];
+  if (c.n < n) {
+    const size_t m = std::max<size_t>(n, 4096);
+    if (c.counters && can_free_now(st)) cudaFree(c.counters);  // leaked while capturing
+    c.counters = nullptr;
+    c.n = 0;
+    if (capture_safe_malloc(reinterpret_cast<void**>(&c.counters), m * sizeof(int), /*zero=*/true) != cudaSuccess)
+      return nullptr;  // no counters: whole tiles only
+    c.n = m;
   }
-  if (ar.ncounters < ncounters) {
-    const size_t n = std::max<size_t>(ncounters, 4096);
-    if (ar.counters && can_free_now(st)) cudaFree(ar.counters);
-    ar.counters = nullptr;
-    ar.ncounters = 0;
-    if (capture_safe_malloc(reinterpret_cast<void**>(&ar.counters), n * sizeof(int), /*zero=*/true) != cudaSuccess)
-      return false;
-    ar.ncounters = n;
-  }
-  *p = ar.partial;
-  *c = ar.counters;
-  return true;
+  return c.counters;
 }
 
 template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR = false>
@@ -675,11 +632,10 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   const int gmax = PAIR ? sms / 2 : sms;
   // Work split: whole tiles round-robin while the last round is well filled; otherwise
   // the last one-to-two rounds of tiles are split by channel chunk over all groups
-  // (stream-K), which needs the partial-tile arena.
+  // (stream-K), which needs the arrival counters.
   a.groups = std::min(tiles, gmax);
   a.dp_tiles = tiles;
   a.sk_units = 0;
-  a.partial = nullptr;
   a.counters = nullptr;
   const int rounds = (tiles + gmax - 1) / gmax;
   const double fill = (double)tiles / ((double)rounds * gmax);
@@ -688,8 +644,7 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   if (sk_mode != 0 && a.CC >= 2 && tiles >= gmax && (fill < kSkFill || sk_mode == 2)) {
     const int dp = std::max(0, tiles / gmax - 1) * gmax;
     const int sk_tiles = tiles - dp;
-    const size_t slab = (size_t)MT * 128 * BN * (PAIR ? 2 : 1);
-    if (sk_arena(st, (size_t)gmax * 2 * slab, (size_t)sk_tiles * (PAIR ? 8 : 4) * 2, &a.partial, &a.counters)) {
+    if ((a.counters = sk_counters(st, (size_t)sk_tiles * (PAIR ? 8 : 4) * 2)) != nullptr) {
       a.groups = gmax;
       a.dp_tiles = dp;
       a.sk_units = sk_tiles * a.CC;
@@ -899,6 +854,7 @@ cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t
                                    const ConvGeom& g, bool split, cudaStream_t st) {
   (void)ldf;
   sw::Args a = sw::make_args(g);
+  a.vec = (g.k_n % 8) == 0 && reinterpret_cast<uintptr_t>(O) % 32 == 0;
   CUtensorMap th, tl;
   cudaError_t e = make_filter_tmap_tapmajor(&th, f_hi, g);
   if (e != cudaSuccess) return e;

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const int64_t P = m0 + warp * 32 + lane;
-    const bool vec = (a.k_n % 4) == 0;
+    const bool vec = (a.k_n % 4) == 0 && reinterpret_cast<uintptr_t>(O) % 16 == 0;
 #pragma unroll 1
     for (int cb = 0; cb < BN / 32; ++cb) {
       uint32_t r[32];

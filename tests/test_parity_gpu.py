@@ -315,3 +315,27 @@ def test_stream_k(orc, monkeypatch, case, prec):
     if cg.last_path() == "tcgen05-shifted":
         # the split changes the fp32 summation order of the split tiles: proof it engaged
         assert not np.array_equal(a, whole)
+
+
+def _offset_tensor4(a, shift):
+    """CUDA leftmost-fastest tensor holding a, starting `shift` floats into its buffer
+    (a user pointer that is only 4-byte aligned)."""
+    a = np.asfortranarray(a, dtype=np.float32)
+    buf = torch.zeros(a.size + shift, dtype=torch.float32, device="cuda")
+    buf[shift:] = torch.from_numpy(a.reshape(-1, order="F")).cuda()
+    d = a.shape
+    return buf[shift:].view(d[3], d[2], d[1], d[0]).permute(3, 2, 1, 0)
+
+
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_unaligned_user_pointers(orc, prec):
+    """F, I and O whose device pointers are only 4-byte aligned: every kernel path must
+    avoid 16/32-byte vector accesses and TMA on them (or stage them) and stay correct."""
+    cp = dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=20, w_i=20, b=3, s=1, p=1)
+    F, I = rand_inputs(cp, 77)
+    ref = orc.conv_gemm(F, I, cp)
+    h_o, w_o = 20, 20
+    for algo in ALGOS:
+        O = _offset_tensor4(np.zeros((64, h_o, w_o, 3), np.float32), 1)
+        cg.conv(_offset_tensor4(F, 1), _offset_tensor4(I, 3), cp, algo=algo, precision=prec, out=O)
+        assert per_output_error(to_host(O), ref, orc.output_scale(F, I, cp)) <= TOL[prec], (algo, cg.last_path())
