@@ -147,6 +147,7 @@ struct DeviceState {
   cudaEvent_t ev_start = nullptr, ev_in = nullptr, ev_comp = nullptr, ev_end = nullptr;
   static constexpr int kSlots = 4;
   cudaEvent_t ev_slot_in[kSlots] = {}, ev_slot_out[kSlots] = {};
+  std::vector<cudaEvent_t> ev_chunk;  // per-chunk "input landed" events (pinned input)
   char* pin = nullptr;  // [kSlots in][kSlots out] bounce slots
   size_t slot_bytes = 0;
   bool ok = false;
@@ -199,7 +200,14 @@ int64_t host_chunk_items(size_t in_item, size_t out_item, int64_t items) {
 static cudaError_t pipeline(DeviceState* d, const HostPipe& io, cudaStream_t compute, std::string* where) {
   cudaError_t e = cudaSuccess;
   const int64_t chunk = io.chunk_items > 0 ? std::min(io.chunk_items, io.items) : io.items;
-  const int64_t nchunks = (io.items + chunk - 1) / chunk;
+  // Chunk plan: equal chunks of about `chunk` items (a size ramp at both ends to shrink
+  // the exposed first H2D / last D2H measured no gain: the call is link-bound).
+  std::vector<int64_t> start;  // first item of each chunk; start.back() == items
+  {
+    const int64_t n = (io.items + chunk - 1) / chunk;
+    for (int64_t k = 0; k <= n; ++k) start.push_back(io.items * k / n);
+  }
+  const int64_t nchunks = (int64_t)start.size() - 1;
   const char* in_h = static_cast<const char*>(io.in_host);
   char* out_h = static_cast<char*>(io.out_host);
   char* in_d = static_cast<char*>(io.in_dev);
@@ -236,18 +244,32 @@ static cudaError_t pipeline(DeviceState* d, const HostPipe& io, cudaStream_t com
   CGB_TRY(cudaStreamWaitEvent(d->d2h, d->ev_start, 0), "stream wait");
   for (const HostPipe::Extra& x : io.extra)  // per-call operands (the filters) go first
     CGB_TRY(cudaMemcpyAsync(x.dev, x.host, x.bytes, cudaMemcpyDefault, d->h2d), "H2D operand");
+  // Pinned input: every chunk's H2D is queued up front, one event per chunk, so the copy
+  // engine never waits for the host to enqueue the next chunk's conv and D2H.
+  if (direct_in) {
+    while ((int64_t)d->ev_chunk.size() < nchunks) {
+      cudaEvent_t ev;
+      CGB_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event create");
+      d->ev_chunk.push_back(ev);
+    }
+    for (int64_t k = 0; k < nchunks; ++k) {
+      const size_t off = (size_t)start[k] * io.in_item, ib = (size_t)(start[k + 1] - start[k]) * io.in_item;
+      CGB_TRY(cudaMemcpyAsync(in_d + off, in_h + off, ib, cudaMemcpyDefault, d->h2d), "H2D input");
+      CGB_TRY(cudaEventRecord(d->ev_chunk[k], d->h2d), "event record");
+    }
+  }
 
   // Pageable buffers: in iteration k the host fills bounce slot k%S with input chunk k
   // and empties the same slot's output half (chunk k-S) in ONE parallel copy job, then
   // queues H2D(k), conv(k), D2H(k); the device runs S chunks behind the host.
   constexpr int S = DeviceState::kSlots;
   auto out_seg = [&](int64_t k) -> CopyPool::Seg {
-    const int64_t i0 = k * chunk, n = std::min(chunk, io.items - i0);
+    const int64_t i0 = start[k], n = start[k + 1] - i0;
     return {out_h + (size_t)i0 * io.out_item, slot_out((int)(k % S)), (size_t)n * io.out_item};
   };
   for (int64_t k = 0; k < nchunks; ++k) {
     const int j = (int)(k % S);
-    const int64_t i0 = k * chunk, n = std::min(chunk, io.items - i0);
+    const int64_t i0 = start[k], n = start[k + 1] - i0;
     const size_t ib = (size_t)n * io.in_item, ob = (size_t)n * io.out_item;
     // ---- host side of the bounce ring
     CopyPool::Seg seg_in{nullptr, nullptr, 0}, seg_out{nullptr, nullptr, 0};
@@ -260,14 +282,15 @@ static cudaError_t pipeline(DeviceState* d, const HostPipe& io, cudaStream_t com
       seg_out = out_seg(k - S);
     }
     pool.copy2(seg_in, seg_out);
-    // ---- H2D
-    CGB_TRY(cudaMemcpyAsync(in_d + (size_t)i0 * io.in_item, direct_in ? in_h + (size_t)i0 * io.in_item : slot_in(j),
-                            ib, cudaMemcpyDefault, d->h2d),
-            "H2D input");
-    if (!direct_in) CGB_TRY(cudaEventRecord(d->ev_slot_in[j], d->h2d), "event record");
-    CGB_TRY(cudaEventRecord(d->ev_in, d->h2d), "event record");
+    // ---- H2D (bounce ring; pinned input was queued above)
+    if (!direct_in) {
+      CGB_TRY(cudaMemcpyAsync(in_d + (size_t)i0 * io.in_item, slot_in(j), ib, cudaMemcpyHostToDevice, d->h2d),
+              "H2D input");
+      CGB_TRY(cudaEventRecord(d->ev_slot_in[j], d->h2d), "event record");
+      CGB_TRY(cudaEventRecord(d->ev_in, d->h2d), "event record");
+    }
     // ---- compute
-    CGB_TRY(cudaStreamWaitEvent(compute, d->ev_in, 0), "stream wait");
+    CGB_TRY(cudaStreamWaitEvent(compute, direct_in ? d->ev_chunk[k] : d->ev_in, 0), "stream wait");
     if ((e = io.compute(io.ctx, i0, n, compute)) != cudaSuccess) {
       *where = "conv";
       return e;

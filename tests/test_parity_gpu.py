@@ -105,8 +105,19 @@ BASELINE_LAYERS = {
     "r50_s2_14": (dict(k_n=512, k_h=3, k_w=3, c_i=512, h_i=14, w_i=14, b=2, s=2, p=1), False),
     "pw_56_64_256": (dict(k_n=256, k_h=1, k_w=1, c_i=64, h_i=56, w_i=56, b=2, s=1, p=0), False),
     "pw_7_512_2048": (dict(k_n=2048, k_h=1, k_w=1, c_i=512, h_i=7, w_i=7, b=2, s=1, p=0), False),
+    "pw_14_1024_256": (dict(k_n=256, k_h=1, k_w=1, c_i=1024, h_i=14, w_i=14, b=2, s=1, p=0), False),
+    "pw_7_2048_512": (dict(k_n=512, k_h=1, k_w=1, c_i=2048, h_i=7, w_i=7, b=2, s=1, p=0), False),
     "stem_224": (dict(k_n=64, k_h=7, k_w=7, c_i=3, h_i=224, w_i=224, b=1, s=2, p=3), True),
     "vgg_conv1": (dict(k_n=64, k_h=3, k_w=3, c_i=3, h_i=224, w_i=224, b=1, s=1, p=1), False),
+    # the rest of the VGG-16 stack (BASELINE configs[4]), b=1
+    "vgg_224_64_64": (dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=224, w_i=224, b=1, s=1, p=1), False),
+    "vgg_112_64_128": (dict(k_n=128, k_h=3, k_w=3, c_i=64, h_i=112, w_i=112, b=1, s=1, p=1), False),
+    "vgg_112_128_128": (dict(k_n=128, k_h=3, k_w=3, c_i=128, h_i=112, w_i=112, b=1, s=1, p=1), False),
+    "vgg_56_128_256": (dict(k_n=256, k_h=3, k_w=3, c_i=128, h_i=56, w_i=56, b=1, s=1, p=1), False),
+    "vgg_56_256_256": (dict(k_n=256, k_h=3, k_w=3, c_i=256, h_i=56, w_i=56, b=1, s=1, p=1), False),
+    "vgg_28_256_512": (dict(k_n=512, k_h=3, k_w=3, c_i=256, h_i=28, w_i=28, b=1, s=1, p=1), False),
+    "vgg_28_512_512": (dict(k_n=512, k_h=3, k_w=3, c_i=512, h_i=28, w_i=28, b=1, s=1, p=1), False),
+    "vgg_14_512_512": (dict(k_n=512, k_h=3, k_w=3, c_i=512, h_i=14, w_i=14, b=1, s=1, p=1), False),
 }
 
 

@@ -44,8 +44,9 @@ def host_memcpy(nbytes=512 << 20):
         ex.shutdown()
     print("cpus", os.cpu_count())
 
-raw_pcie()
-host_memcpy()
+if not os.environ.get("HB_SKIP_RAW"):
+    raw_pcie()
+    host_memcpy()
 layers = bench.LAYERS if len(sys.argv) < 2 else [l for l in bench.LAYERS if l[0] in sys.argv[1:]]
 tensors = bench.make_layer_tensors(cg, torch, layers, 128, 0, 1)
 host = []
@@ -57,7 +58,7 @@ def pinned(a):
     t = torch.empty(a.size, dtype=torch.float32, pin_memory=True)
     v = t.numpy(); v[:] = a.reshape(-1, order="F")
     return v.reshape(a.shape, order="F"), t
-for mb in (sys.argv[1:] and ["8"]) or ("4", "8", "16", "32", "64"):
+for mb in os.environ.get("HB_MB", "4,8,16,32").split(","):
     os.environ["CGB_HOST_CHUNK_MB"] = mb
     for kind in ("pinned", "pageable"):
         tot = 0.0
