@@ -42,6 +42,7 @@ constexpr int PRODUCER_WARPS = CGB_SW_PWARPS;
 #define CGB_SW_UPI 1
 #endif
 constexpr int UPI = CGB_SW_UPI;  // window units each producer warp keeps in flight
+
 // Warp roles: producers, the window forwarder (CTA pairs: one thread turns the local
 // "window staged" barrier into one cluster-scope arrive on the leader's barrier per
 // chunk), the filter TMA warp, the MMA issuer, 4 epilogue warps. The sub-partition
@@ -259,7 +260,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t ph = (it / A_SLOTS) & 1;
         // WAR on this CTA's own window: completion of the reading UMMAs is all that is
         // needed, so a CTA-scope wait (a cluster-scope acquire compiles to an L1 flush).
-        mbar_wait(&a_empty[s], ph ^ 1);
+        // The first unit's loads are issued before the wait, so their latency overlaps it.
+        bool slot_free = false;
         const uint32_t base_hi = smem_u32(a_slot(s, 0));
         const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
         const int cmax = a.c_i - cc * BK;
@@ -281,10 +283,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
 #pragma unroll
           for (int q = 0; q < UPI; ++q) load_rows(src[q], ok[q], cmax, v[q]);
+          if (!slot_free) {
+            mbar_wait(&a_empty[s], ph ^ 1);
+            slot_free = true;
+          }
 #pragma unroll
           for (int q = 0; q < UPI; ++q)
             if (q == 0 || u + q * PRODUCER_WARPS < units) store_rows(row[q], v[q], base_hi + off[q], base_lo + off[q]);
         }
+        if (!slot_free) mbar_wait(&a_empty[s], ph ^ 1);  // no unit this chunk: still in phase order
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
