@@ -169,7 +169,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_init(&a_empty[s], 1);
       }
       for (int s = 0; s < B_STAGES; ++s) {
-        mbar_init(&b_full[s], 1);
+        // TMA-skipping profile mode: both ranks arrive, so neither runs phases ahead
+        mbar_init(&b_full[s], (PAIR && (a.dbg & 8)) ? 2 : 1);
         mbar_init(&b_empty[s], 1);
       }
       for (int s = 0; s < 2; ++s) {
@@ -327,7 +328,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int tap = 0; tap < a.taps; ++tap) {
             mbar_wait_spin(&b_empty[bs], bph ^ 1);  // WAR on own smem: CTA scope suffices
             if (a.dbg & 8) {
-              if (rank == 0) mbar_arrive(&b_full[bs]);
+              if (PAIR) mbar_arrive_cluster(lead_b_full + bs * 8);
+              else mbar_arrive(&b_full[bs]);
             } else {
               if (rank == 0) mbar_arrive_expect_tx(&b_full[bs], bytes);
               const uint32_t stage_off = (uint32_t)bs * C::NS * C::B_TILE;
@@ -625,7 +627,9 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   constexpr int pair_rows = (PAIR ? 2 : 1) * MT * 128;
   a.m_tiles = (int32_t)((a.Mp + pair_rows - 1) / pair_rows);
   a.n_tiles = (a.k_n + BN - 1) / BN;
-  const size_t smem = base_smem;
+  size_t smem = base_smem;
+  if (const char* pad = getenv("CGB_SW_SMEM_PAD"))  // profiling: shrink the L1 carve-out
+    smem = std::max<size_t>(smem, (size_t)atoi(pad) * 1024);
   auto kern = sw_conv_kernel<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
   if (getenv("CGB_SW_VERBOSE"))
     fprintf(stderr, "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d smem=%.1fKB\n", MT, BN, (int)SPLIT,
