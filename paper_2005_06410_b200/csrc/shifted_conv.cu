@@ -711,9 +711,11 @@ static Args make_args(const ConvGeom& g) {
   const char* dbg = getenv("CGB_DEBUG_SW");
   a.dbg = dbg ? atoi(dbg) : 0;
   a.stats = nullptr;
-  if (a.dbg & 64) {
-    if (!g_stats) capture_safe_malloc(reinterpret_cast<void**>(&g_stats), 1024 * 16 * sizeof(unsigned long long));
-    a.stats = g_stats;
+  if (a.dbg & 64) {  // 8 launch slots of 1024 CTAs x 16 counters (slot = launch index % 8)
+    if (!g_stats)
+      capture_safe_malloc(reinterpret_cast<void**>(&g_stats), 8 * 1024 * 16 * sizeof(unsigned long long), true);
+    static int slot = 0;
+    a.stats = g_stats + (size_t)(slot++ % 8) * 1024 * 16;
   }
   return a;
 }
@@ -890,9 +892,11 @@ cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t
 // b_full), segments, epilogue wait/busy cycles, then %globaltimer stamps (ns): entry,
 // MMA loop start, MMA loop end, epilogue end, exit, producers end; and the SM id.
 extern "C" int cgb_debug_sw_stats(unsigned long long* host, int n_cta) {
+  // n_cta > 1024: all 8 launch slots (8 x 1024 x 16 counters); host == NULL: zero them
   if (!cgb::sw::g_stats) return -1;
-  return cudaMemcpy(host, cgb::sw::g_stats, (size_t)n_cta * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
-                 cudaSuccess
+  const size_t n = n_cta > 1024 ? (size_t)8 * 1024 * 16 : (size_t)n_cta * 16;
+  if (!host) return cudaMemset(cgb::sw::g_stats, 0, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+  return cudaMemcpy(host, cgb::sw::g_stats, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess
              ? 0
              : -1;
 }
