@@ -74,6 +74,9 @@ def split_range(count, rank, nranks):
 
 
 def peaks():
+    """Roofline denominators. HBM: MEASURED_PEAKS.json. TF32: cuBLAS TF32 measured on this
+    pool the way MEASURED_PEAKS.json measures bf16 (tools/measure_tf32.py ->
+    profiles/tf32_peak.json); bf16/2 when that file is absent."""
     p = {"hbm_gbs": 6545.6, "bf16_tflops": 1627.7, "src": "MEASURED_PEAKS.json"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -82,7 +85,17 @@ def peaks():
         p["bf16_tflops"] = float(m["bf16_tflops"])
     except Exception:
         p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
-    p["tf32_tflops"] = p["bf16_tflops"] / 2.0  # dense TF32 = 1/2 dense BF16 on tcgen05
+    p["tf32_from_bf16"] = p["bf16_tflops"] / 2.0  # dense TF32 = 1/2 dense BF16 on tcgen05
+    p["tf32_tflops"] = p["tf32_from_bf16"]
+    p["tf32_src"] = f"bf16_tflops/2 from {p['src']} (of measured)"
+    try:
+        with open(os.path.join(ROOT, "profiles", "tf32_peak.json")) as f:
+            t = json.load(f)
+        p["tf32_tflops"] = float(t["tf32_tflops"])
+        p["tf32_src"] = ("measured: cuBLAS TF32 8192^3 burst on this pool (profiles/tf32_peak.json, "
+                         "tools/measure_tf32.py; same method as MEASURED_PEAKS.json's bf16)")
+    except Exception:
+        pass
     return p
 
 
@@ -456,7 +469,12 @@ def run_gpu_arm(args, world, rank, local):
                    "parallelism": f"batch-sharded dp{world}, no collective in the timed region"},
         "roofline": {"bound": "tensor", "achieved": hm["achieved_tflops"], "peak": pk["tf32_tflops"],
                      "unit": "TFLOP/s", "frac": hm["achieved_tflops"] / pk["tf32_tflops"], "traffic": traffic,
-                     "peak_src": f"dense TF32 = bf16_tflops/2 from {pk['src']} (of measured)",
+                     "peak_src": pk["tf32_src"],
+                     "frac_vs_other_peaks": {
+                         "bf16_tflops/2 of MEASURED_PEAKS.json": hm["achieved_tflops"] / pk["tf32_from_bf16"],
+                         "nominal dense TF32 1100 (B200_PROFILING.md table)": hm["achieved_tflops"] / 1100.0,
+                         "tcgen05 UMMA microbenchmark 1151 @1.9 GHz (tools/umma_bench.cu)":
+                             hm["achieved_tflops"] / 1151.0},
                      "per_layer": hm["layers"]},
         "cpu_baseline": cpu,
         "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
