@@ -68,9 +68,9 @@ struct Args {
   int64_t Mp;         // padded output rows Hq*Wq*b
   int32_t Mp32;       // same, 32-bit (shifted_supported guarantees < 2^31 - tile)
   int64_t plane;      // h_i*w_i
-  // Work split (see SegIter): tiles [0, dp_tiles) whole and round-robin over the
-  // `groups` CTAs (pairs: clusters); the channel-chunk units of the remaining tiles
-  // (sk_units = their count x CC) in one contiguous, balanced range per group.
+  // Work split (see seg_get): the channel-chunk units of tiles [0, sk_units / CC) in one
+  // contiguous, balanced range per group (stream-K), then dp_tiles whole tiles
+  // round-robin over the `groups` CTAs (pairs: clusters).
   int32_t dp_tiles, sk_units, groups;
   int* counters;      // [sk tile][ranks*4 epilogue warps][arrived, written]; zero between launches
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
@@ -79,28 +79,34 @@ struct Args {
                       //   4 = skip epilogue stores, 8 = skip filter TMA
 };
 
-// Segment sequence of one group: its whole (data-parallel) tiles gid, gid+G, ... below
-// dp_tiles, then the pieces of its stream-K unit range [sk_begin(gid), sk_begin(gid+1))
-// cut at tile boundaries. Every role of the kernel walks the same sequence; the state
-// is just the segment index j (registers are the binding resource of this kernel).
+// Segment sequence of one group: first the pieces of its stream-K unit range
+// [sk_begin(gid), sk_begin(gid+1)) over tiles [0, sk_tiles), cut at tile boundaries;
+// then its whole (data-parallel) tiles sk_tiles + gid, + G, ... Split pieces come first
+// so every group ends on plain whole-tile stores (a final split piece would leave the
+// wait-for-the-other-piece and its red.adds exposed at the end of the kernel). Every
+// role walks the same sequence; the state is just the segment index j (registers are
+// the binding resource of this kernel).
 CGB_DEV int64_t sk_begin(const Args& a, int g) { return (int64_t)g * a.sk_units / a.groups; }
 CGB_DEV bool seg_get(const Args& a, int gid, int j, int& tile, int& cc0, int& cc1) {
+  const int ub = (int)sk_begin(a, gid), ue = (int)sk_begin(a, gid + 1);
+  const int npieces = ue > ub ? (ue - 1) / a.CC - ub / a.CC + 1 : 0;
+  if (j < npieces) {
+    const int t0 = ub / a.CC + j;
+    const int us = j == 0 ? ub : t0 * a.CC;
+    tile = t0;
+    cc0 = us - t0 * a.CC;
+    cc1 = min(a.CC, ue - t0 * a.CC);
+    return true;
+  }
+  j -= npieces;
   const int ndp = gid < a.dp_tiles ? (a.dp_tiles - gid + a.groups - 1) / a.groups : 0;
   if (j < ndp) {
-    tile = gid + j * a.groups;
+    tile = a.sk_units / a.CC + gid + j * a.groups;
     cc0 = 0;
     cc1 = a.CC;
     return true;
   }
-  j -= ndp;
-  const int ub = (int)sk_begin(a, gid), ue = (int)sk_begin(a, gid + 1);
-  const int t0 = ub / a.CC + j;  // stream-K tile index of piece j
-  const int us = j == 0 ? ub : t0 * a.CC;
-  if (us >= ue) return false;
-  tile = a.dp_tiles + t0;
-  cc0 = us - t0 * a.CC;
-  cc1 = min(a.CC, ue - t0 * a.CC);
-  return true;
+  return false;
 }
 // group whose stream-K range holds unit x
 CGB_DEV int sk_group_of(const Args& a, int x) {
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int* cnt = nullptr;
       bool add = false;
       if (!whole) {
-        const int stl = tile - a.dp_tiles;
+        const int stl = tile;  // stream-K tiles are tiles [0, sk_tiles)
         cnt = a.counters + ((size_t)stl * (PAIR ? 8 : 4) + rank * 4 + sub) * 2;
         int old = 0;
         if (lane == 0) old = atomicAdd(cnt, 1);
