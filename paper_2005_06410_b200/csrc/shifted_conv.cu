@@ -763,8 +763,13 @@ static const Cand kCands[] = {
     {1, 256, 0, 1, 3, 0}, {1, 256, 1, 1, 2, 0},
     // CTA pairs with one window slot
     {2, 64, 0, 1, 8, 1},  {1, 64, 0, 1, 8, 1},  {2, 128, 0, 1, 4, 1}, {1, 128, 0, 1, 4, 1}, {1, 256, 0, 1, 3, 1},
+    // deep filter rings: only for filter-stream-heavy layers (BN = 256 and >= 2 filter
+    // tiles, e.g. 7x7/14x14 512->512: 3-9% faster); elsewhere the extra shared memory
+    // costs L1 and measured slower (dispatch)
+    {1, 256, 0, 2, 9, 1}, {1, 256, 0, 2, 4, 1},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
+constexpr int kFirstDeepCand = 36;
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st) {
@@ -807,6 +812,8 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(33, 2, 128, false, 1, 4, true)
     CGB_SW_CASE(34, 1, 128, false, 1, 4, true)
     CGB_SW_CASE(35, 1, 256, false, 1, 3, true)
+    CGB_SW_CASE(36, 1, 256, false, 2, 9, true)
+    CGB_SW_CASE(37, 1, 256, false, 2, 4, true)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -852,7 +859,12 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
       }
     }
     if (const char* f = getenv("CGB_SW_MT")) mt_max = atoi(f);  // profiling override
-    for (int i = 0; i < kNumCands; ++i) {
+    const bool deep_first = bn == 256 && n_tiles >= 2;
+    for (int k = 0; k < kNumCands; ++k) {
+      // deep-ring candidates first for filter-heavy layers, never otherwise
+      const int i = deep_first ? (k < kNumCands - kFirstDeepCand ? kFirstDeepCand + k : k - (kNumCands - kFirstDeepCand))
+                               : k;
+      if (!deep_first && i >= kFirstDeepCand) continue;
       const Cand& c = kCands[i];
       if (c.bn != bn || c.split != (int)split || c.mt > mt_max || c.pair != want_pair) continue;
       if (pass % 2 == 0 && c.as != 2) continue;

@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, int a_shift_rows, int
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;          // 64 KB of A rows
   uint8_t* sb = smem + 65536;  // B
-  __shared__ uint64_t bar, bar2;
+  __shared__ uint64_t bar, bar2, rot[16];
   __shared__ uint32_t tmem_holder;
   const int tid = threadIdx.x;
   for (int i = tid; i < (65536 + N * 128) / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 1.0f / (1 + (i & 7));
@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, int a_shift_rows, int
   if (tid == 0) {
     mbar_init(&bar, 1);
     mbar_init(&bar2, 1);
+    for (int i = 0; i < 16; ++i) mbar_init(&rot[i], 1);
     fence_mbar_init();
   }
   if (tid < 32) tmem_alloc(&tmem_holder, N < 32 ? 64 : 2 * N);
@@ -44,8 +45,8 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, int a_shift_rows, int
       const uint64_t bdd = bvary ? bd + (uint64_t)((it & 3) * 2) : bd;
       const uint32_t dd = dvary ? tmem + (it & 1) * N : tmem;
       mma_tf32(dd, ad, bdd, idesc, it > 1);
-      const int cevery = a_tmem_unused >> 4;
-      if (cevery && (it % cevery) == cevery - 1) mma_commit(&bar2);
+      const int cevery = (a_tmem_unused >> 4) & 255, nrot = a_tmem_unused >> 12;
+      if (cevery && (it % cevery) == cevery - 1) mma_commit(nrot ? &rot[(it / cevery) % nrot] : &bar2);
     }
     mma_commit(&bar);
     mbar_wait(&bar, 0);
@@ -90,5 +91,10 @@ int main() {
   run<128>(it, 1, 1, "A,B vary, D alt, commit every 8", 3 | (8 << 4));
   run<64>(it, 1, 1, "A,B vary, D alt, commit every 16", 3 | (16 << 4));
   run<256>(it, 1, 1, "A,B vary, commit every 4", 1 | (4 << 4));
+  // commit every 8 MMAs (N=128): same barrier vs a ring of 2/3/4/8 barriers
+  for (int nrot : {0, 2, 3, 4, 8, 16})
+    run<128>(it, 1, 0, nrot ? "commit every 8, ring of barriers" : "commit every 8, one barrier", 3 | (8 << 4) | (nrot << 12));
+  for (int nrot : {0, 3, 8})
+    run<256>(it, 1, 0, nrot ? "commit every 4, ring" : "commit every 4, one barrier", 3 | (4 << 4) | (nrot << 12));
   return 0;
 }
