@@ -483,6 +483,8 @@ def run_gpu_arm(args, world, rank, local):
         "clocks": clk,
         "modes": {m: {"value": v["value"], "ms_per_step": v["ms_per_step"],
                       "tf32_frac": v["achieved_tflops"] / pk["tf32_tflops"],
+                      # 3xTF32 issues three TF32 MMAs per product: its own roofline is P_TF32/3
+                      "frac_of_own_roofline": v["achieved_tflops"] / (pk["tf32_tflops"] / (3 if m == "3xtf32" else 1)),
                       "per_layer_tflops": {l["layer"]: l["tflops"] for l in v["layers"]}} for m, v in modes.items()},
     }
     print(json.dumps(line), flush=True)
