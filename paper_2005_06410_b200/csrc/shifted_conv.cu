@@ -3,7 +3,8 @@
 // The reference materialises (explicit path, im2col.hpp:77-120) or packs on the fly
 // (fused path, pack_b_im2col im2col.hpp:177-262) k_h*k_w shifted copies of every
 // input element. On B200 the copies are unnecessary: index output pixels in the
-// *padded* plane, m' = i_h + H_q*(i_w + W_q*i_b) with H_q = h_i + 2p, W_q = w_i + 2p
+// *padded* plane, m' = i_h + H_q*(i_w + W_q*i_b) with H_q = h_i + p, W_q = w_i + p at
+// stride 1 -- neighbouring columns and images share their zero padding (plane_period) --
 // (rows with i_h >= h_o or i_w >= w_o are computed and discarded), and the A operand
 // of filter tap (kh, kw) is the padded input window shifted by d = kh + H_q*kw rows.
 // A K-major, 128B-swizzled shared-memory window (one 128-byte row = 32 channels of one
@@ -72,7 +73,7 @@ struct Args {
   // contiguous, balanced range per group (stream-K), then dp_tiles whole tiles
   // round-robin over the `groups` CTAs (pairs: clusters).
   int32_t dp_tiles, sk_units, groups;
-  int* counters;      // [sk tile][ranks*4 epilogue warps][arrived, written]; zero between launches
+  int* counters;      // [sk tile][ranks*4 epilogue warps] pieces written; zero between launches
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   unsigned long long* stats;  // per-CTA cycle counters when dbg & 64 (profiling only)
   int32_t dbg;        // profiling switches (CGB_DEBUG_SW): 1 = producers skip loads, 2 = skip MMAs,
@@ -484,24 +485,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       unsigned long long e1 = (a.dbg & 64) ? clock64() : 0;
       if (a.dbg & 64) epi_wait += e1 - e0;
       tc_fence_after();
-      // ---- stream-K piece of a split tile. The host enables stream-K only when every
-      // group's range holds >= CC units, so a split tile has exactly two pieces. Each
-      // (CTA rank, epilogue warp) of both pieces arrives once: the first stores its rows
-      // into O like a whole tile and publishes "written"; the second waits for that and
-      // red.adds its rows into O (fire-and-forget, no loads). O = p0 + p1 rounded once,
-      // the same value whichever piece finishes first.
+      // ---- stream-K piece of a split tile. Groups' unit ranges are contiguous, so every
+      // group whose range meets the tile holds exactly one piece of it, and the pieces are
+      // ordered by channel chunk. They are combined in a FIXED order, highest chunks first:
+      // the piece of rank 0 (the last group touching the tile, for which it is the FIRST
+      // segment, so it finishes early) stores its rows; the piece of rank r waits until r
+      // pieces have been written and red.adds its rows into O. O = ((p_0 + p_1) + p_2)...,
+      // bitwise independent of timing. Waits only point at pieces that are earlier
+      // segments of higher-numbered groups, so the chain always resolves. The last piece
+      // resets the counter for the next launch.
       const bool whole = cc0 == 0 && cc1 == a.CC;
       int* cnt = nullptr;
       bool add = false;
+      int prank = 0, npieces = 1;
       if (!whole) {
-        const int stl = tile;  // stream-K tiles are tiles [0, sk_tiles)
-        cnt = a.counters + ((size_t)stl * (PAIR ? 8 : 4) + rank * 4 + sub) * 2;
-        int old = 0;
-        if (lane == 0) old = atomicAdd(cnt, 1);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        add = old == 1;
+        const int u0 = tile * a.CC;  // stream-K tiles are tiles [0, sk_tiles)
+        const int g_hi = sk_group_of(a, u0 + a.CC - 1);
+        prank = g_hi - gid;
+        npieces = g_hi - sk_group_of(a, u0) + 1;
+        cnt = a.counters + (size_t)tile * (PAIR ? 8 : 4) + rank * 4 + sub;
+        add = prank > 0;
         if (add)
-          while (ld_acquire_gpu(cnt + 1) < 1) {
+          while (ld_acquire_gpu(cnt) < prank) {
           }
       }
 #pragma unroll 1
@@ -544,13 +549,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       if (!whole) {
-        if (!add) {
-          __threadfence();  // each lane's rows before the "written" count
+        if (prank + 1 < npieces) {
+          __threadfence();  // each lane's rows (stores or reds) before the "written" count
           __syncwarp();
-          if (lane == 0) atomicAdd(cnt + 1, 1);
+          if (lane == 0) atomicAdd(cnt, 1);
         } else if (lane == 0) {
-          cnt[0] = 0;  // both pieces arrived and the first has written: reset for the next launch
-          cnt[1] = 0;
+          *cnt = 0;  // last piece: every other piece has written and stopped polling
         }
       }
       tc_fence_before();
@@ -657,11 +661,15 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   const int rounds = (tiles + gmax - 1) / gmax;
   const double fill = (double)tiles / ((double)rounds * gmax);
   const int sk_mode = sk_env();
-  // Stream-K needs >= CC units per group (two pieces per split tile): tiles >= groups.
-  if (sk_mode != 0 && a.CC >= 2 && tiles >= gmax && (fill < kSkFill || sk_mode == 2)) {
+  // Stream-K only for the last one-to-two rounds of at least one tile per group: every
+  // split tile adds a red.add pass over its rows (L2 atomics), which measured slower than
+  // the idle SMs it saves when ALL tiles would be split (1-round layers: 7x7, 14x14).
+  // The fixup itself handles any number of pieces per tile (sk_mode 2 forces it).
+  const bool sk_ok = sk_mode == 2 ? (int64_t)tiles * a.CC >= 2 * gmax : tiles >= gmax;
+  if (sk_mode != 0 && a.CC >= 2 && sk_ok && (fill < kSkFill || sk_mode == 2)) {
     const int dp = std::max(0, tiles / gmax - 1) * gmax;
     const int sk_tiles = tiles - dp;
-    if ((a.counters = sk_counters(st, (size_t)sk_tiles * (PAIR ? 8 : 4) * 2)) != nullptr) {
+    if ((a.counters = sk_counters(st, (size_t)sk_tiles * (PAIR ? 8 : 4))) != nullptr) {
       a.groups = gmax;
       a.dp_tiles = dp;
       a.sk_units = sk_tiles * a.CC;
@@ -696,6 +704,27 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
 
 static unsigned long long* g_stats = nullptr;
 
+// Period of the padded plane along one spatial dimension (rows per column / columns per
+// image). Phase a of a stride-s dimension holds input n = s*q + a - p at position q;
+// output o reads phase a at q = o + kh/s for the taps kh = a (mod s). Consecutive
+// columns (images) may SHARE their zero padding: a read past the period wraps into the
+// next column's leading zero rows, which is exact as long as (i) every wrapped read lands
+// in those zeros (q_max(a) - period < z_lead(a)), (ii) no row that a valid output reads
+// holds data beyond the period (period > min(q_last(a), q_max(a))), and (iii) the valid
+// outputs fit. For stride 1, k=3, p=1 this is n_i + 1 instead of n_i + 2 (7x7: 64 padded
+// rows per image instead of 81); for stride 2 it equals the unshared n_o + 1.
+static int32_t plane_period(int64_t n_i, int64_t n_o, int64_t k, int64_t s, int64_t p) {
+  int64_t per = n_o;
+  for (int64_t a = 0; a < std::min(s, k); ++a) {
+    const int64_t z_lead = p > a ? (p - a + s - 1) / s : 0;
+    const int64_t q_last = (n_i - 1 + p - a) / s;  // last data row of phase a
+    const int64_t q_max = n_o - 1 + (k - 1 - a) / s;  // last row a valid output reads
+    per = std::max(per, std::min(q_last, q_max) + 1);
+    per = std::max(per, q_max - z_lead + 1);
+  }
+  return (int32_t)std::min(per, n_o + (k - 1) / s);
+}
+
 static Args make_args(const ConvGeom& g) {
   Args a;
   a.k_n = (int32_t)g.k_n; a.k_h = (int32_t)g.k_h; a.k_w = (int32_t)g.k_w; a.c_i = (int32_t)g.c_i;
@@ -705,8 +734,8 @@ static Args make_args(const ConvGeom& g) {
   a.nph_h = (int32_t)std::min(g.s, g.k_h);
   a.nph_w = (int32_t)std::min(g.s, g.k_w);
   a.NPH = a.nph_h * a.nph_w;
-  a.Hq = (int32_t)(g.h_o + (g.k_h - 1) / g.s);
-  a.Wq = (int32_t)(g.w_o + (g.k_w - 1) / g.s);
+  a.Hq = plane_period(g.h_i, g.h_o, g.k_h, g.s, g.p);
+  a.Wq = plane_period(g.w_i, g.w_o, g.k_w, g.s, g.p);
   a.dmax = (a.k_h - 1) / a.s + a.Hq * ((a.k_w - 1) / a.s);
   a.CC = (a.c_i + BK - 1) / BK;
   a.taps = a.k_h * a.k_w;
@@ -731,14 +760,16 @@ static Args make_args(const ConvGeom& g) {
 // Domain: filters through the tap-major TMA map (k_n % 4 == 0), at least half a channel
 // chunk, stride <= 2 (<= 4 phase planes), and a padded plane that wastes < 70% rows.
 static double padded_waste(const ConvGeom& g) {
-  const double hq = (double)(g.h_o + (g.k_h - 1) / g.s), wq = (double)(g.w_o + (g.k_w - 1) / g.s);
+  const double hq = sw::plane_period(g.h_i, g.h_o, g.k_h, g.s, g.p);
+  const double wq = sw::plane_period(g.w_i, g.w_o, g.k_w, g.s, g.p);
   return hq * wq / (double)(g.h_o * g.w_o);
 }
 
 bool shifted_supported(const ConvGeom& g) {
   if (g.s > 2 || g.k_n % 4 != 0 || g.c_i < 16 || g.k_h * g.k_w > 64) return false;
   if (padded_waste(g) > 1.7) return false;
-  const int64_t hq = g.h_o + (g.k_h - 1) / g.s, wq = g.w_o + (g.k_w - 1) / g.s;
+  const int64_t hq = sw::plane_period(g.h_i, g.h_o, g.k_h, g.s, g.p);
+  const int64_t wq = sw::plane_period(g.w_i, g.w_o, g.k_w, g.s, g.p);
   const int64_t dmax = (g.k_h - 1) / g.s + hq * ((g.k_w - 1) / g.s);
   const int64_t mp = hq * wq * g.b;
   return dmax <= 256 && mp < (int64_t(1) << 30) && g.c_i * g.h_i * g.w_i * g.b < (int64_t(1) << 31);
@@ -842,13 +873,13 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     // Whole tiles cost ceil(tiles / groups) rounds; with stream-K (tiles >= groups, a
     // last round < 90% full, >= 2 channel chunks) the work spreads evenly: tiles / groups.
     // Tile times relative to MT = 2 measured on B200 (bigger M tiles reuse each filter
-    // tile over more rows): MT 1 -> 0.65, 2 -> 1, 4 -> 1.8.
+    // tile over more rows): MT 1 -> 0.62, 2 -> 1, 4 -> 1.8.
     const int units = want_pair ? 2 : 1;
     const int gmax = want_pair ? sms / 2 : sms;
     int mt_max = 1;
     double best = 1e30;
     for (int mt = 4; mt >= 1; mt /= 2) {
-      const double tt = mt == 4 ? 1.8 : (mt == 2 ? 1.0 : 0.65);
+      const double tt = mt == 4 ? 1.8 : (mt == 2 ? 1.0 : 0.62);
       const int tiles = (int)((a.Mp + units * mt * 128 - 1) / (units * mt * 128)) * n_tiles;
       const int rounds = (tiles + gmax - 1) / gmax;
       const bool sk = sk_env() != 0 && a.CC >= 2 && tiles >= gmax && (double)tiles / (rounds * gmax) < kSkFill;

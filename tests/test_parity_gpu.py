@@ -277,7 +277,11 @@ VARIANT_CASES = [
     (dict(k_n=64, k_h=1, k_w=1, c_i=64, h_i=28, w_i=28, b=2, s=2, p=0), "tcgen05-shifted"),
     (dict(k_n=48, k_h=2, k_w=2, c_i=24, h_i=17, w_i=17, b=2, s=2, p=0), "tcgen05-shifted"),
     (dict(k_n=256, k_h=3, k_w=3, c_i=96, h_i=28, w_i=28, b=1, s=2, p=1), "tcgen05-shifted"),
-    (dict(k_n=128, k_h=5, k_w=5, c_i=32, h_i=12, w_i=12, b=2, s=1, p=2), "tcgen05-gather"),
+    # 5x5 p=2: the shared-padding plane (14 rows per column instead of 16) keeps it shifted
+    (dict(k_n=128, k_h=5, k_w=5, c_i=32, h_i=12, w_i=12, b=2, s=1, p=2), "tcgen05-shifted"),
+    (dict(k_n=64, k_h=7, k_w=7, c_i=32, h_i=6, w_i=6, b=3, s=1, p=3), "tcgen05-gather"),
+    # pad > k-1 and asymmetric periods: wrapped reads land in shared zero rows
+    (dict(k_n=64, k_h=3, k_w=2, c_i=32, h_i=11, w_i=9, b=3, s=1, p=2), "tcgen05-shifted"),
     (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=20, w_i=20, b=2, s=3, p=1), "tcgen05-gather"),
 ]
 
@@ -304,13 +308,19 @@ SK_CASES = [
     dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=28, w_i=28, b=24, s=1, p=1),
     dict(k_n=128, k_h=3, k_w=3, c_i=64, h_i=56, w_i=56, b=24, s=2, p=1),
     dict(k_n=96, k_h=3, k_w=3, c_i=80, h_i=20, w_i=20, b=48, s=1, p=1),
+    # fewer tiles than SM pairs, many channel chunks, stream-K forced (CGB_SW_SK=2): every
+    # tile is split into several pieces, combined in the fixed highest-chunk-first order
+    dict(k_n=256, k_h=3, k_w=3, c_i=512, h_i=7, w_i=7, b=48, s=1, p=1, force=True),
+    dict(k_n=512, k_h=3, k_w=3, c_i=256, h_i=14, w_i=14, b=48, s=2, p=1, force=True),
 ]
 
 
 @pytest.mark.parametrize("case", range(len(SK_CASES)))
 @pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
 def test_stream_k(orc, monkeypatch, case, prec):
-    cp = SK_CASES[case]
+    cp = dict(SK_CASES[case])
+    if cp.pop("force", False):
+        monkeypatch.setenv("CGB_SW_SK", "2")
     F, I = rand_inputs(cp, 300 + case)
     ref = orc.conv_gemm(F, I, cp)
     scale = orc.output_scale(F, I, cp)
