@@ -25,20 +25,25 @@ using namespace cgb;
 constexpr int SLOT = 9216;  // raw slot: 32 channels x (64 + 4) floats, 128-byte aligned
 
 struct P {
-  int h_i, w_i, c_i, b, s, p, Hq, Wq, nph, CC, nb;
-  long items;  // LDG items (one h phase each); TMA items = items / nph (both h phases)
+  int h_i, w_i, c_i, b, s, p, Hq, Wq, nph, CC;
+  int ncol;        // padded columns per window (one CTA tile's window)
+  int nb_ldg;      // 32-lane units per column and phase (LDG mode)
+  int nb_tma;      // TMA boxes per column and phase (32*s + 4 rows each)
+  int windows;     // total windows
+  long items;      // total LDG items (for the byte count)
 };
 
-// pa < 0: TMA item (both h phases of 32 rows); bx = 32-row block of the column
-__device__ __forceinline__ void decode(const P& a, int it, int& bb, int& wq, int& cc, int& pa, int& pc, int& bx,
-                                       bool tma) {
-  if (tma) pa = -1;
-  else { pa = (int)(it % a.nph); it /= a.nph; }
-  pc = (int)(it % a.nph); it /= a.nph;
-  bx = (int)(it % a.nb); it /= a.nb;
-  cc = (int)(it % a.CC); it /= a.CC;
-  wq = (int)(it % a.Wq); it /= a.Wq;
-  bb = (int)it;
+// Window-major order like the conv kernel: a CTA stages window w (ncol consecutive
+// padded columns) for chunk cc, items in row order within each w-phase plane.
+__device__ __forceinline__ void item_ldg(const P& a, int w, int j, int& col, int& pc, int& bx) {
+  bx = j % a.nb_ldg; j /= a.nb_ldg;
+  col = w * a.ncol + j % a.ncol; j /= a.ncol;
+  pc = j;
+}
+__device__ __forceinline__ void item_tma(const P& a, int w, int j, int& col, int& pc, int& bx) {
+  bx = j % a.nb_tma; j /= a.nb_tma;
+  col = w * a.ncol + j % a.ncol; j /= a.ncol;
+  pc = j;
 }
 
 template <int NW, int RS>
@@ -66,28 +71,33 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     if (warp == NW) {
       if (lane == 0) {
         int k = 0;
-        const long n = a.items / a.nph;
-        for (long it = first; it < n; it += step, ++k) {
-          // item k -> consumer warp k % NW, which owns slots [w*SPW, (w+1)*SPW)
-          const int j = k / NW, slot = (k % NW) * SPW + j % SPW;
-          mbar_wait(&empty[slot], ((j / SPW) & 1) ^ 1);
-          int bb, wq, cc, pa, pc, bx;
-          decode(a, (int)it, bb, wq, cc, pa, pc, bx, true);
-          // dim-0 box starts must be 16-byte aligned: start 4-aligned below, 4 extra rows
-          const int h0 = 32 * a.s * bx - a.p, h0a = h0 >= 0 ? h0 & ~3 : -((-h0 + 3) & ~3);
-          mbar_arrive_expect_tx(&full[slot], 32 * (32 * a.s + 4) * 4);
-          tma_load_4d(smem_u32(ring + slot * SLOT), &tm, &full[slot], h0a, a.s * wq + pc - a.p, 32 * cc, bb);
-        }
+        const int ipw = a.nph * a.ncol * a.nb_tma;
+        for (int w = blockIdx.x; w < a.windows; w += gridDim.x)
+          for (int cc = 0; cc < a.CC; ++cc)
+            for (int jj = 0; jj < ipw; ++jj, ++k) {
+              const int j = k / NW, slot = (k % NW) * SPW + j % SPW;
+              mbar_wait(&empty[slot], ((j / SPW) & 1) ^ 1);
+              int col, pc, bx;
+              item_tma(a, w, jj, col, pc, bx);
+              const int wq = col % a.Wq, bb = col / a.Wq;
+              // dim-0 box starts must be 16-byte aligned: start 4-aligned below, 4 extra rows
+              const int h0 = 32 * a.s * bx - a.p, h0a = h0 >= 0 ? h0 & ~3 : -((-h0 + 3) & ~3);
+              mbar_arrive_expect_tx(&full[slot], 32 * (32 * a.s + 4) * 4);
+              tma_load_4d(smem_u32(ring + slot * SLOT), &tm, &full[slot], h0a, a.s * wq + pc - a.p, 32 * cc, bb);
+            }
       }
     } else {
-      int k = warp;
-      const long n = a.items / a.nph;
-      for (long it = first + (long)warp * step; it < n; it += step * NW, k += NW) {
+      int k = 0;
+      const int ipw = a.nph * a.ncol * a.nb_tma;
+      for (int w = blockIdx.x; w < a.windows; w += gridDim.x)
+        for (int cc = 0; cc < a.CC; ++cc)
+          for (int jj = 0; jj < ipw; ++jj, ++k) {
+        if (k % NW != warp) continue;
         const int j = k / NW, slot = warp * SPW + j % SPW;
         mbar_wait(&full[slot], (j / SPW) & 1);
         const uint32_t dst = smem_u32(win + warp * 4096);
-        int bb, wq, cc, pa, pc, bx;
-        decode(a, (int)it, bb, wq, cc, pa, pc, bx, true);
+        int col, pc, bx;
+        item_tma(a, w, jj, col, pc, bx);
         const int h0 = 32 * a.s * bx - a.p, h0a = h0 >= 0 ? h0 & ~3 : -((-h0 + 3) & ~3);
         const int RW = 32 * a.s + 4;  // raw row (one channel) in floats
         const uint32_t src = smem_u32(ring + slot * SLOT) + (h0 - h0a) * 4;
@@ -126,25 +136,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     }
   } else if (warp < NW) {
     int k = 0;
-    for (long it = first + (long)warp * step; it < a.items; it += step * NW, ++k) {
-      int bb, wq, cc, pa, pc, bx;
-      decode(a, (int)it, bb, wq, cc, pa, pc, bx, false);
-      const int h = a.s * (32 * bx + lane) + pa - a.p, w = a.s * wq + pc - a.p;
-      const bool ok = (unsigned)h < (unsigned)a.h_i && (unsigned)w < (unsigned)a.w_i;
-      const float* src = I + ((long)bb * a.c_i + 32L * cc) * plane + (long)w * a.h_i + h;
-      if (mode == 2) {
-        const long nx = it + step * NW;
-        if (nx < a.items) {
-          int b2, w2, c2, pa2, pc2, bx2;
-          decode(a, (int)nx, b2, w2, c2, pa2, pc2, bx2, false);
-          const int h0 = max(a.s * 32 * bx2 + pa2 - a.p, 0), ww = a.s * w2 + pc2 - a.p;
-          if ((unsigned)ww < (unsigned)a.w_i) {
-            const float* q = I + ((long)b2 * a.c_i + 32L * c2 + lane) * plane + (long)ww * a.h_i + h0;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
-            if (a.s == 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(q + 32));
-          }
-        }
-      }
+    const int ipw = a.nph * a.ncol * a.nb_ldg;
+    for (int w = blockIdx.x; w < a.windows; w += gridDim.x)
+      for (int cc = 0; cc < a.CC; ++cc)
+        for (int jj = warp; jj < ipw; jj += NW, ++k) {
+      int col, pc, bx;
+      item_ldg(a, w, jj, col, pc, bx);
+      const int wq = col % a.Wq, bb = col / a.Wq;
+      // kernel lane mapping: stride 2 -> lanes cover 16 rows x both h phases = 32 consecutive h
+      const int row = a.s == 2 ? (lane & 7) + 8 * (lane >> 4) + 16 * bx : lane + 32 * bx;
+      const int pa = a.s == 2 ? (lane >> 3) & 1 : 0;
+      const int h = a.s * row + pa - a.p, wi = a.s * wq + pc - a.p;
+      const bool ok = row < a.Hq && (unsigned)h < (unsigned)a.h_i && (unsigned)wi < (unsigned)a.w_i;
+      const float* src = I + ((long)bb * a.c_i + 32L * cc) * plane + (long)wi * a.h_i + h;
       float v[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) v[c] = ok ? __ldg(src + (long)c * plane) : 0.0f;
@@ -201,7 +205,7 @@ void run(const char* name, const float* I, P a, int mode, int mtimes) {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     best = ms < best ? ms : best;
   }
-  const double bytes = (double)a.items * 4096;
+  const double bytes = (double)a.items * a.nph * a.Hq * 128;  // useful window rows
   printf("%-28s NW=%2d RS=%2d smem=%3zu KB: %8.1f us  %7.1f GB/s of window  checksum %llx  (%s)\n", name, NW, RS,
          smem / 1024, best * 1e3, bytes / (best * 1e-3) / 1e9, h0, cudaGetErrorString(cudaGetLastError()));
   cudaFree(sum);
@@ -212,22 +216,25 @@ int main(int argc, char** argv) {
   // default: the stride-2 56->28 c128 layer at b=128; "s1" selects 56x56 c64 stride 1
   setvbuf(stdout, nullptr, _IONBF, 0);
   const bool s1 = argc > 1 && argv[1][0] == 's' && argv[1][1] == '1';
+  const int batch = getenv("FB_BATCH") ? atoi(getenv("FB_BATCH")) : 128;
   P a;
-  if (s1) { a.h_i = a.w_i = 56; a.c_i = 64; a.b = 128; a.s = 1; a.p = 1; a.Hq = 57; a.Wq = 57; a.nb = 2; }
-  else    { a.h_i = a.w_i = 56; a.c_i = 128; a.b = 128; a.s = 2; a.p = 1; a.Hq = 29; a.Wq = 29; a.nb = 1; }
+  if (s1) { a.h_i = a.w_i = 56; a.c_i = 64; a.b = batch; a.s = 1; a.p = 1; a.Hq = 57; a.Wq = 57; a.ncol = 11;
+             a.nb_ldg = 2; a.nb_tma = 2; }
+  else    { a.h_i = a.w_i = 56; a.c_i = 128; a.b = batch; a.s = 2; a.p = 1; a.Hq = 29; a.Wq = 29; a.ncol = 6;
+             a.nb_ldg = 2; a.nb_tma = 1; }
   a.nph = a.s; a.CC = a.c_i / 32;
-  a.items = (long)a.b * a.Wq * a.CC * a.nph * a.nph * a.nb;
+  a.windows = a.b * a.Wq / a.ncol;
+  a.items = (long)a.windows * a.CC * a.nph * a.ncol;  // (column, w-phase, chunk) triples
   const size_t n = (size_t)a.h_i * a.w_i * a.c_i * a.b;
   float* I;
   cudaMalloc(&I, n * 4);
   std::vector<float> h(n);
   for (size_t i = 0; i < n; ++i) h[i] = (float)((i * 2654435761u) % 1000) * 1e-3f;
   cudaMemcpy(I, h.data(), n * 4, cudaMemcpyHostToDevice);
-  printf("geometry %s: input %.1f MB, %ld items (%.1f MB of window)\n", s1 ? "56x56 c64 s1" : "56->28 c128 s2",
-         n * 4 / 1e6, a.items, a.items * 4096 / 1e6);
+  printf("geometry %s: input %.1f MB, %.1f MB of window\n", s1 ? "56x56 c64 s1" : "56->28 c128 s2", n * 4 / 1e6,
+         a.items * a.nph * a.Hq * 128 / 1e6);
   if (!only_tma) {
     run<12, 12>("LDG (mode 0)", I, a, 0, 5);
-    run<12, 12>("LDG + L2 prefetch (mode 2)", I, a, 2, 5);
     run<16, 16>("LDG (mode 0)", I, a, 0, 5);
   }
   run<12, 12>("TMA ring (mode 1)", I, a, 1, 5);
