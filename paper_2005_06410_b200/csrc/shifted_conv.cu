@@ -39,10 +39,6 @@ constexpr int BK = 32;
 #define CGB_SW_PWARPS 12
 #endif
 constexpr int PRODUCER_WARPS = CGB_SW_PWARPS;
-#ifndef CGB_SW_UPI
-#define CGB_SW_UPI 1
-#endif
-constexpr int UPI = CGB_SW_UPI;  // window units each producer warp keeps in flight
 
 // Warp roles: producers, the window forwarder (CTA pairs: one thread turns the local
 // "window staged" barrier into one cluster-scope arrive on the leader's barrier per
@@ -133,7 +129,9 @@ struct Cfg {
 // from the peer's window at the same shared-memory offset, B split into two halves of
 // BN/2 filters (one per CTA), accumulators in both CTAs' TMEM. Per SM this halves the
 // filter-tile TMA traffic, the B operand reads and the B staging footprint.
-template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR>
+// UPI: window units each producer warp keeps in flight (loads of UPI units issued before
+// any of them is stored). 2 for the staging-bound configurations, else 1 (registers).
+template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR, int UPI>
 __global__ void __launch_bounds__(THREADS, 1)
     sw_conv_kernel(const __grid_constant__ CUtensorMap tmap_hi, const __grid_constant__ CUtensorMap tmap_lo,
                    const float* __restrict__ I, float* __restrict__ O, Args a, uint32_t a_slot_bytes) {
@@ -625,7 +623,7 @@ static int* sk_counters(cudaStream_t st, size_t n) {
   return c.counters;
 }
 
-template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR = false>
+template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR, int UPI>
 cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, Args a,
                        cudaStream_t st) {
   using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
@@ -640,10 +638,10 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   size_t smem = base_smem;
   if (const char* pad = getenv("CGB_SW_SMEM_PAD"))  // profiling: shrink the L1 carve-out
     smem = std::max<size_t>(smem, (size_t)atoi(pad) * 1024);
-  auto kern = sw_conv_kernel<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
+  auto kern = sw_conv_kernel<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR, UPI>;
   if (getenv("CGB_SW_VERBOSE"))
-    fprintf(stderr, "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d smem=%.1fKB\n", MT, BN, (int)SPLIT,
-            A_SLOTS, B_STAGES, (int)PAIR, smem / 1024.0);
+    fprintf(stderr, "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d smem=%.1fKB\n", MT, BN,
+            (int)SPLIT, A_SLOTS, B_STAGES, (int)PAIR, UPI, smem / 1024.0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -780,71 +778,83 @@ namespace sw {
 // B stages). A config is skipped when its shared memory does not fit
 // (launch_cfg -> cudaErrorNotSupported).
 struct Cand {
-  int mt, bn, split, as, bs, pair;
+  int mt, bn, split, as, bs, pair, upi;
 };
 static const Cand kCands[] = {
     // CTA pairs (cta_group::2): B halves per CTA -> deeper filter pipelines
-    {4, 64, 0, 2, 8, 1},  {2, 64, 0, 2, 8, 1},  {1, 64, 0, 2, 8, 1},  {2, 64, 1, 1, 6, 1},  {1, 64, 1, 1, 6, 1},
-    {2, 128, 0, 2, 6, 1}, {1, 128, 0, 2, 4, 1}, {1, 128, 0, 2, 3, 1}, {2, 128, 1, 1, 4, 1}, {1, 128, 1, 1, 3, 1},
-    {2, 256, 0, 2, 4, 1}, {1, 256, 0, 2, 3, 1}, {1, 256, 0, 2, 2, 1}, {1, 256, 1, 1, 2, 1},
+    {4, 64, 0, 2, 8, 1, 1},  {2, 64, 0, 2, 8, 1, 1},  {1, 64, 0, 2, 8, 1, 1},  {2, 64, 1, 1, 6, 1, 1},
+    {1, 64, 1, 1, 6, 1, 1},  {2, 128, 0, 2, 6, 1, 1}, {1, 128, 0, 2, 4, 1, 1}, {1, 128, 0, 2, 3, 1, 1},
+    {2, 128, 1, 1, 4, 1, 1}, {1, 128, 1, 1, 3, 1, 1}, {2, 256, 0, 2, 4, 1, 1}, {1, 256, 0, 2, 3, 1, 1},
+    {1, 256, 0, 2, 2, 1, 1}, {1, 256, 1, 1, 2, 1, 1},
     // single CTA
-    {4, 64, 0, 2, 6, 0},  {2, 64, 0, 2, 6, 0},  {1, 64, 0, 2, 6, 0},  {2, 64, 1, 1, 4, 0},  {1, 64, 1, 1, 4, 0},
-    {2, 128, 0, 2, 4, 0}, {2, 128, 0, 1, 4, 0}, {1, 128, 0, 2, 4, 0}, {1, 128, 0, 1, 4, 0}, {2, 128, 1, 1, 3, 0},
-    {1, 128, 1, 1, 3, 0}, {2, 256, 0, 2, 3, 0}, {2, 256, 0, 1, 3, 0}, {1, 256, 0, 2, 3, 0}, {1, 256, 0, 2, 2, 0},
-    {1, 256, 0, 1, 3, 0}, {1, 256, 1, 1, 2, 0},
+    {4, 64, 0, 2, 6, 0, 1},  {2, 64, 0, 2, 6, 0, 1},  {1, 64, 0, 2, 6, 0, 1},  {2, 64, 1, 1, 4, 0, 1},
+    {1, 64, 1, 1, 4, 0, 1},  {2, 128, 0, 2, 4, 0, 1}, {2, 128, 0, 1, 4, 0, 1}, {1, 128, 0, 2, 4, 0, 1},
+    {1, 128, 0, 1, 4, 0, 1}, {2, 128, 1, 1, 3, 0, 1}, {1, 128, 1, 1, 3, 0, 1}, {2, 256, 0, 2, 3, 0, 1},
+    {2, 256, 0, 1, 3, 0, 1}, {1, 256, 0, 2, 3, 0, 1}, {1, 256, 0, 2, 2, 0, 1}, {1, 256, 0, 1, 3, 0, 1},
+    {1, 256, 1, 1, 2, 0, 1},
     // CTA pairs with one window slot
-    {2, 64, 0, 1, 8, 1},  {1, 64, 0, 1, 8, 1},  {2, 128, 0, 1, 4, 1}, {1, 128, 0, 1, 4, 1}, {1, 256, 0, 1, 3, 1},
+    {2, 64, 0, 1, 8, 1, 1},  {1, 64, 0, 1, 8, 1, 1},  {2, 128, 0, 1, 4, 1, 1}, {1, 128, 0, 1, 4, 1, 1},
+    {1, 256, 0, 1, 3, 1, 1},
     // deep filter rings: only for filter-stream-heavy layers (BN = 256 and >= 2 filter
     // tiles, e.g. 7x7/14x14 512->512: 3-9% faster); elsewhere the extra shared memory
     // costs L1 and measured slower (dispatch)
-    {1, 256, 0, 2, 9, 1}, {1, 256, 0, 2, 4, 1},
+    {1, 256, 0, 2, 9, 1, 1}, {1, 256, 0, 2, 4, 1, 1},
+    // two window units in flight per producer warp: staging-bound layers only (BN = 64,
+    // or stride 2 with BN <= 128: 56x56 64->64 3% and 56->28 128 8% faster; slower where
+    // the MMA or the filter stream binds)
+    {4, 64, 0, 2, 8, 1, 2}, {2, 64, 0, 2, 8, 1, 2}, {1, 128, 0, 2, 4, 1, 2}, {2, 128, 0, 2, 6, 1, 2},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
+constexpr int kFirstUpi2Cand = 38;
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st) {
-#define CGB_SW_CASE(IDX, MT, BN, SP, AS, BS, PR) \
-  case IDX: return launch_cfg<MT, BN, SP, AS, BS, PR>(th, tl, I, O, a, st);
+#define CGB_SW_CASE(IDX, MT, BN, SP, AS, BS, PR, U) \
+  case IDX: return launch_cfg<MT, BN, SP, AS, BS, PR, U>(th, tl, I, O, a, st);
   switch (i) {
-    CGB_SW_CASE(0, 4, 64, false, 2, 8, true)
-    CGB_SW_CASE(1, 2, 64, false, 2, 8, true)
-    CGB_SW_CASE(2, 1, 64, false, 2, 8, true)
-    CGB_SW_CASE(3, 2, 64, true, 1, 6, true)
-    CGB_SW_CASE(4, 1, 64, true, 1, 6, true)
-    CGB_SW_CASE(5, 2, 128, false, 2, 6, true)
-    CGB_SW_CASE(6, 1, 128, false, 2, 4, true)
-    CGB_SW_CASE(7, 1, 128, false, 2, 3, true)
-    CGB_SW_CASE(8, 2, 128, true, 1, 4, true)
-    CGB_SW_CASE(9, 1, 128, true, 1, 3, true)
-    CGB_SW_CASE(10, 2, 256, false, 2, 4, true)
-    CGB_SW_CASE(11, 1, 256, false, 2, 3, true)
-    CGB_SW_CASE(12, 1, 256, false, 2, 2, true)
-    CGB_SW_CASE(13, 1, 256, true, 1, 2, true)
-    CGB_SW_CASE(14, 4, 64, false, 2, 6, false)
-    CGB_SW_CASE(15, 2, 64, false, 2, 6, false)
-    CGB_SW_CASE(16, 1, 64, false, 2, 6, false)
-    CGB_SW_CASE(17, 2, 64, true, 1, 4, false)
-    CGB_SW_CASE(18, 1, 64, true, 1, 4, false)
-    CGB_SW_CASE(19, 2, 128, false, 2, 4, false)
-    CGB_SW_CASE(20, 2, 128, false, 1, 4, false)
-    CGB_SW_CASE(21, 1, 128, false, 2, 4, false)
-    CGB_SW_CASE(22, 1, 128, false, 1, 4, false)
-    CGB_SW_CASE(23, 2, 128, true, 1, 3, false)
-    CGB_SW_CASE(24, 1, 128, true, 1, 3, false)
-    CGB_SW_CASE(25, 2, 256, false, 2, 3, false)
-    CGB_SW_CASE(26, 2, 256, false, 1, 3, false)
-    CGB_SW_CASE(27, 1, 256, false, 2, 3, false)
-    CGB_SW_CASE(28, 1, 256, false, 2, 2, false)
-    CGB_SW_CASE(29, 1, 256, false, 1, 3, false)
-    CGB_SW_CASE(30, 1, 256, true, 1, 2, false)
-    CGB_SW_CASE(31, 2, 64, false, 1, 8, true)
-    CGB_SW_CASE(32, 1, 64, false, 1, 8, true)
-    CGB_SW_CASE(33, 2, 128, false, 1, 4, true)
-    CGB_SW_CASE(34, 1, 128, false, 1, 4, true)
-    CGB_SW_CASE(35, 1, 256, false, 1, 3, true)
-    CGB_SW_CASE(36, 1, 256, false, 2, 9, true)
-    CGB_SW_CASE(37, 1, 256, false, 2, 4, true)
+    CGB_SW_CASE(0, 4, 64, false, 2, 8, true, 1)
+    CGB_SW_CASE(1, 2, 64, false, 2, 8, true, 1)
+    CGB_SW_CASE(2, 1, 64, false, 2, 8, true, 1)
+    CGB_SW_CASE(3, 2, 64, true, 1, 6, true, 1)
+    CGB_SW_CASE(4, 1, 64, true, 1, 6, true, 1)
+    CGB_SW_CASE(5, 2, 128, false, 2, 6, true, 1)
+    CGB_SW_CASE(6, 1, 128, false, 2, 4, true, 1)
+    CGB_SW_CASE(7, 1, 128, false, 2, 3, true, 1)
+    CGB_SW_CASE(8, 2, 128, true, 1, 4, true, 1)
+    CGB_SW_CASE(9, 1, 128, true, 1, 3, true, 1)
+    CGB_SW_CASE(10, 2, 256, false, 2, 4, true, 1)
+    CGB_SW_CASE(11, 1, 256, false, 2, 3, true, 1)
+    CGB_SW_CASE(12, 1, 256, false, 2, 2, true, 1)
+    CGB_SW_CASE(13, 1, 256, true, 1, 2, true, 1)
+    CGB_SW_CASE(14, 4, 64, false, 2, 6, false, 1)
+    CGB_SW_CASE(15, 2, 64, false, 2, 6, false, 1)
+    CGB_SW_CASE(16, 1, 64, false, 2, 6, false, 1)
+    CGB_SW_CASE(17, 2, 64, true, 1, 4, false, 1)
+    CGB_SW_CASE(18, 1, 64, true, 1, 4, false, 1)
+    CGB_SW_CASE(19, 2, 128, false, 2, 4, false, 1)
+    CGB_SW_CASE(20, 2, 128, false, 1, 4, false, 1)
+    CGB_SW_CASE(21, 1, 128, false, 2, 4, false, 1)
+    CGB_SW_CASE(22, 1, 128, false, 1, 4, false, 1)
+    CGB_SW_CASE(23, 2, 128, true, 1, 3, false, 1)
+    CGB_SW_CASE(24, 1, 128, true, 1, 3, false, 1)
+    CGB_SW_CASE(25, 2, 256, false, 2, 3, false, 1)
+    CGB_SW_CASE(26, 2, 256, false, 1, 3, false, 1)
+    CGB_SW_CASE(27, 1, 256, false, 2, 3, false, 1)
+    CGB_SW_CASE(28, 1, 256, false, 2, 2, false, 1)
+    CGB_SW_CASE(29, 1, 256, false, 1, 3, false, 1)
+    CGB_SW_CASE(30, 1, 256, true, 1, 2, false, 1)
+    CGB_SW_CASE(31, 2, 64, false, 1, 8, true, 1)
+    CGB_SW_CASE(32, 1, 64, false, 1, 8, true, 1)
+    CGB_SW_CASE(33, 2, 128, false, 1, 4, true, 1)
+    CGB_SW_CASE(34, 1, 128, false, 1, 4, true, 1)
+    CGB_SW_CASE(35, 1, 256, false, 1, 3, true, 1)
+    CGB_SW_CASE(36, 1, 256, false, 2, 9, true, 1)
+    CGB_SW_CASE(37, 1, 256, false, 2, 4, true, 1)
+    CGB_SW_CASE(38, 4, 64, false, 2, 8, true, 2)
+    CGB_SW_CASE(39, 2, 64, false, 2, 8, true, 2)
+    CGB_SW_CASE(40, 1, 128, false, 2, 4, true, 2)
+    CGB_SW_CASE(41, 2, 128, false, 2, 6, true, 2)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -891,19 +901,31 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     }
     if (const char* f = getenv("CGB_SW_MT")) mt_max = atoi(f);  // profiling override
     const bool deep_first = bn == 256 && n_tiles >= 2;
-    for (int k = 0; k < kNumCands; ++k) {
-      // deep-ring candidates first for filter-heavy layers, never otherwise
-      const int i = deep_first ? (k < kNumCands - kFirstDeepCand ? kFirstDeepCand + k : k - (kNumCands - kFirstDeepCand))
-                               : k;
-      if (!deep_first && i >= kFirstDeepCand) continue;
+    // staging-bound layers (stride-2 windows with BN <= 128, or BN = 64) first try the
+    // candidates with two units in flight per producer warp
+    const bool upi2 = (a.s == 2 && bn <= 128) || bn == 64;
+    const int nupi2 = kNumCands - kFirstUpi2Cand;
+    for (int k = 0; k < kNumCands + nupi2; ++k) {
+      int i;
+      if (k < nupi2) {
+        if (!upi2) continue;
+        i = kFirstUpi2Cand + k;
+      } else {
+        const int k2 = k - nupi2;
+        if (k2 >= kFirstUpi2Cand) break;
+        // deep-ring candidates first for filter-heavy layers, never otherwise
+        i = deep_first ? (k2 < kFirstUpi2Cand - kFirstDeepCand ? kFirstDeepCand + k2 : k2 - (kFirstUpi2Cand - kFirstDeepCand))
+                       : k2;
+        if (!deep_first && i >= kFirstDeepCand) continue;
+      }
       const Cand& c = kCands[i];
       if (c.bn != bn || c.split != (int)split || c.mt > mt_max || c.pair != want_pair) continue;
       if (pass % 2 == 0 && c.as != 2) continue;
       cudaError_t e = launch_cand(i, th, tl, I, O, a, st);
       if (e != cudaErrorNotSupported) {
         if (getenv("CGB_SW_VERBOSE"))
-          fprintf(stderr, "[cgb] shifted cand %d: MT=%d BN=%d split=%d A=%d B=%d pair=%d\n", i, c.mt, c.bn, c.split,
-                  c.as, c.bs, c.pair);
+          fprintf(stderr, "[cgb] shifted cand %d: MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d\n", i, c.mt, c.bn,
+                  c.split, c.as, c.bs, c.pair, c.upi);
         return e;
       }
     }
