@@ -770,7 +770,7 @@ bool shifted_supported(const ConvGeom& g) {
   const int64_t wq = sw::plane_period(g.w_i, g.w_o, g.k_w, g.s, g.p);
   const int64_t dmax = (g.k_h - 1) / g.s + hq * ((g.k_w - 1) / g.s);
   const int64_t mp = hq * wq * g.b;
-  return dmax <= 256 && mp < (int64_t(1) << 30) && g.c_i * g.h_i * g.w_i * g.b < (int64_t(1) << 31);
+  return dmax <= 2048 && mp < (int64_t(1) << 30) && g.c_i * g.h_i * g.w_i * g.b < (int64_t(1) << 31);
 }
 
 namespace sw {

@@ -280,6 +280,8 @@ VARIANT_CASES = [
     # 5x5 p=2: the shared-padding plane (14 rows per column instead of 16) keeps it shifted
     (dict(k_n=128, k_h=5, k_w=5, c_i=32, h_i=12, w_i=12, b=2, s=1, p=2), "tcgen05-shifted"),
     (dict(k_n=64, k_h=7, k_w=7, c_i=32, h_i=6, w_i=6, b=3, s=1, p=3), "tcgen05-gather"),
+    # wide image: window halo (2 + 2*151 rows) beyond 256 rows (VGG 224x224 layers)
+    (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=150, w_i=150, b=1, s=1, p=1), "tcgen05-shifted"),
     # pad > k-1 and asymmetric periods: wrapped reads land in shared zero rows
     (dict(k_n=64, k_h=3, k_w=2, c_i=32, h_i=11, w_i=9, b=3, s=1, p=2), "tcgen05-shifted"),
     (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=20, w_i=20, b=2, s=3, p=1), "tcgen05-gather"),
