@@ -17,7 +17,9 @@ for l in bench.LAYERS:
         print("missing", rep); continue
     s = subprocess.run([sys.executable, os.path.join(ROOT, "tools/ncu_summary.py"), rep], capture_output=True, text=True).stdout
     open(os.path.join(prof, f"{RND}_{l[0]}_ncu_raw.txt"), "w").write(s)
-    h = subprocess.run([sys.executable, os.path.join(ROOT, "tools/ncu_hot.py"), rep, "40"], capture_output=True, text=True).stdout
+    h = subprocess.run([sys.executable, os.path.join(ROOT, "tools/ncu_stalls.py"), rep, "40"], capture_output=True, text=True).stdout
+    h += "\n-- per CUDA source line --\n"
+    h += subprocess.run([sys.executable, os.path.join(ROOT, "tools/ncu_lines.py"), rep, "25"], capture_output=True, text=True).stdout
     open(os.path.join(prof, f"{RND}_{l[0]}_ncu_hot_sass.txt"), "w").write(h)
     rd = wr = None
     for line in s.splitlines():
