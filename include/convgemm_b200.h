@@ -7,6 +7,7 @@
  *   cgb_conv_im2col_gemm    <- convgemm::conv_im2col_gemm<float> conv.hpp:60-74  (explicit: im2col, then gemm)
  *   cgb_conv                <- both of the above, plus the precision selector the B200 path adds
  *   cgb_im2col              <- convgemm::im2col<float>           im2col.hpp:77-120 (explicit lowered matrix)
+ *   cgb_gemm                <- convgemm::gemm<float> over a MatrixSource gemm.hpp:46-105 (fc layers, bench.cpp:140-153)
  *   cgb_output_dims         <- convgemm::output_dims             conv_params.hpp:27-36
  *   cgb_gemm_dims           <- convgemm::gemm_dims               conv_params.hpp:40-43
  *   cgb_im2col_workspace_bytes <- convgemm::im2col_workspace_bytes im2col.hpp:36-39
@@ -101,6 +102,13 @@ cgb_status cgb_conv_im2col_gemm(const float* F, const float* I, const cgb_conv_p
 /* Explicit lowered matrix B (k x n, column-major, leading dimension ldb >= k),
  * bit-identical to im2col<float>. Rows k..ldb-1 of each column are zero-filled. */
 cgb_status cgb_im2col(const float* I, const cgb_conv_params* cp, float* B, int64_t ldb, void* stream);
+
+/* C (m x n) = A (m x k) * B (k x n), column-major, O overwritten (the reference
+ * zero-fills C before gemm, bench.cpp:149-151). Dense A and C (lda == ldc == m),
+ * ldb >= k. Runs the explicit-path tensor-core (or FFMA) kernel with B as the lowered
+ * matrix; precision as for cgb_conv. */
+cgb_status cgb_gemm(int precision, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                    int64_t m, int64_t n, int64_t k, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- host-pointer entry point: synchronous, reference semantics ----
  * Copies F and I host->device, runs cgb_conv, copies O device->host, syncs.

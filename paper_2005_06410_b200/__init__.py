@@ -30,7 +30,9 @@ __all__ = [
     "AllocationFailure", "BlockingParams", "ConvParams", "DimensionMismatch", "InvalidGeometry",
     "conv", "conv_gemm", "conv_im2col_gemm", "convgemm_scratch_bytes", "empty_tensor4", "gemm_dims",
     "im2col", "im2col_workspace_bytes", "output_dims", "scratch_peak_bytes", "scratch_reset_peak",
-    "scratch_set_limit", "kernel_launch_count", "last_path", "PRECISIONS", "ALGOS",
+    "scratch_set_limit", "kernel_launch_count", "last_path", "PRECISIONS", "ALGOS", "gemm",
+    "IoError", "conv_workspace_bytes", "LayerSpec", "ModelSpec", "LayerResult", "ParseError", "UnknownLayerKind", "parse_model",
+    "model_workspace_bytes", "run_inference", "write_csv",
 ]
 
 ALGOS = {"explicit": 0, "im2col": 0, "fused": 1, "convgemm": 1}
@@ -49,6 +51,10 @@ class DimensionMismatch(ValueError):
 
 class AllocationFailure(MemoryError):
     """convgemm::AllocationFailure (types.hpp:23)."""
+
+
+class IoError(OSError):
+    """convgemm::IoError (types.hpp:25-29)."""
 
 
 class DeviceError(RuntimeError):
@@ -135,8 +141,11 @@ def convgemm_scratch_bytes(blocking: BlockingParams | None = None) -> int:
     return (bp.mc * bp.kc + bp.kc * bp.nc) * 4
 
 
-def conv_workspace_bytes(cp, algo: str = "fused", precision: str = "auto") -> int:
-    return lib.cgb_conv_workspace_bytes(ALGOS[algo], PRECISIONS[precision], ctypes.byref(ConvParams.of(cp).c()))
+def conv_workspace_bytes(cp, algo: str = "fused", precision: str = "auto", external_b: bool = False) -> int:
+    """Device workspace one call takes (filter split + B-hat for the explicit path);
+    ``external_b``: B-hat is the caller's (``gemm``), so only the filter part counts."""
+    a = ALGOS["fused"] if external_b else ALGOS[algo]  # same filter part, no B-hat
+    return lib.cgb_conv_workspace_bytes(a, PRECISIONS[precision], ctypes.byref(ConvParams.of(cp).c()))
 
 
 def scratch_peak_bytes() -> int:
@@ -247,6 +256,42 @@ def conv_im2col_gemm(F, I, cp, blocking: BlockingParams | None = None, threads: 
     return conv(F, I, cp, "explicit", precision, out)
 
 
+def gemm(A, B, blocking: BlockingParams | None = None, threads: int = 1, precision: str = "auto", out=None):
+    """C = A @ B for column-major (Fortran-ordered) float32 matrices, the reference's
+    ``gemm`` binding (bindings.cpp:200-210; gemm.hpp:46-105 over a MatrixSource). Runs as
+    a 1x1 convolution over 1x1 images through ``cgb_gemm``: CUDA tensors on the current
+    stream, numpy arrays synchronously (copied through the device)."""
+    import torch
+    _validate_blocking(blocking)
+    host = not _is_torch(A)
+    if host:
+        An, Bn = np.asarray(A), np.asarray(B)
+        if An.dtype == np.float64 or Bn.dtype == np.float64:
+            raise Unsupported("float64 runs on the CPU reference only; the B200 operator is float32")
+        A = torch.from_numpy(np.ascontiguousarray(An.astype(np.float32).T)).cuda().t()
+        B = torch.from_numpy(np.ascontiguousarray(Bn.astype(np.float32).T)).cuda().t()
+    if A.dim() != 2 or B.dim() != 2:
+        raise DimensionMismatch("gemm operands must be matrices")
+    m, k = A.shape
+    k2, n = B.shape
+    if k2 != k:
+        raise DimensionMismatch(f"gemm inner dimensions disagree: {m}x{k} times {k2}x{n}")
+    for x, nm in ((A, "a"), (B, "b")):
+        if not x.is_cuda or x.dtype != torch.float32 or x.stride(0) != 1:
+            raise ValueError(f"{nm} must be a column-major (Fortran-ordered) float32 CUDA matrix")
+    if A.stride(1) != m:
+        raise DimensionMismatch("a must be dense (leading dimension == rows)")
+    C = out if out is not None else torch.empty((n, m), device=A.device, dtype=torch.float32).t()
+    if tuple(C.shape) != (m, n) or C.stride(0) != 1 or C.stride(1) != m:
+        raise DimensionMismatch("output must be a dense column-major m x n float32 matrix")
+    st = torch.cuda.current_stream(A.device).cuda_stream
+    _check(lib.cgb_gemm(PRECISIONS[precision], A.data_ptr(), m, B.data_ptr(), max(B.stride(1), k), C.data_ptr(), m,
+                        m, n, k, None, 0, st))
+    if host:
+        return np.asfortranarray(C.cpu().numpy())
+    return C
+
+
 def im2col(I, cp, threads: int = 1, ldb: int | None = None, out=None):
     """Lowered matrix B (k x n, column-major) from the device kernel; bit-exact with im2col<float>."""
     import torch
@@ -266,3 +311,8 @@ def im2col(I, cp, threads: int = 1, ldb: int | None = None, out=None):
     if host:
         return np.asfortranarray(Bt.cpu().numpy())
     return Bt
+
+
+from .simulator import (  # noqa: E402  (the simulator builds on the entry points above)
+    LayerResult, LayerSpec, ModelSpec, ParseError, UnknownLayerKind, model_workspace_bytes, parse_model,
+    run_inference, write_csv)

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("CGB_LIB_OVERRIDE") or os.path.join(HERE, "libconvgemm
 SYMBOLS = (
     "cgb_output_dims", "cgb_gemm_dims", "cgb_im2col_workspace_bytes", "cgb_validate_blocking",
     "cgb_conv_workspace_bytes", "cgb_conv", "cgb_conv_gemm", "cgb_conv_im2col_gemm", "cgb_im2col",
-    "cgb_conv_host", "cgb_scratch_current_bytes", "cgb_scratch_peak_bytes", "cgb_scratch_reset_peak",
+    "cgb_gemm", "cgb_conv_host", "cgb_scratch_current_bytes", "cgb_scratch_peak_bytes", "cgb_scratch_reset_peak",
     "cgb_scratch_set_limit", "cgb_scratch_release", "cgb_last_error", "cgb_version",
     "cgb_kernel_launch_count", "cgb_last_path", "cgb_debug_sw_stats",
 )
@@ -51,6 +51,7 @@ def _load() -> ctypes.CDLL:
         "cgb_conv_gemm": (st, [vp, vp, cpp, bpp, ctypes.c_int, vp, ctypes.c_int, vp]),
         "cgb_conv_im2col_gemm": (st, [vp, vp, cpp, bpp, ctypes.c_int, vp, ctypes.c_int, vp]),
         "cgb_im2col": (st, [vp, cpp, vp, i64, vp]),
+        "cgb_gemm": (st, [ctypes.c_int, vp, i64, vp, i64, vp, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]),
         "cgb_conv_host": (st, [ctypes.c_int, ctypes.c_int, vp, vp, cpp, vp, vp]),
         "cgb_scratch_current_bytes": (ctypes.c_uint64, []),
         "cgb_scratch_peak_bytes": (ctypes.c_uint64, []),

@@ -258,19 +258,20 @@ int64_t cgb_conv_workspace_bytes(int algo, int precision, const cgb_conv_params*
   return pl.f_bytes + pl.b_bytes;
 }
 
-cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, const cgb_conv_params* cp, float* O,
-                    void* workspace, size_t workspace_bytes, void* stream) {
-  ConvGeom g;
-  cgb_status st = make_geom(cp, &g);
-  if (st) return st;
-  if (algo != CGB_ALGO_EXPLICIT && algo != CGB_ALGO_FUSED) return fail(CGB_INVALID_ARGUMENT, "unknown algo");
-  if (precision < CGB_PREC_AUTO || precision > CGB_PREC_FFMA)
-    return fail(CGB_INVALID_ARGUMENT, "unknown precision");
-  if (!F || !I || !O) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
-  if ((st = check_device_limits(g))) return st;
+// The operator body behind cgb_conv and cgb_gemm. Bext != NULL: the lowered matrix B
+// (k x n, leading dimension ldb_ext) is the caller's (gemm over a MatrixSource,
+// gemm.hpp:100-105): the explicit path without the im2col step or its workspace.
+static cgb_status conv_impl(int algo, int precision, const float* F, const float* I, const ConvGeom& g, float* O,
+                            void* workspace, size_t workspace_bytes, void* stream, const float* Bext,
+                            int64_t ldb_ext) {
+  cgb_status st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int prec = resolve_precision(precision, g);
-  const Plan pl = make_plan(algo, prec, g, F);
+  Plan pl = make_plan(algo, prec, g, F);
+  if (Bext) {
+    pl.b_bytes = 0;
+    pl.ldb = ldb_ext;
+  }
   const size_t need = (size_t)(pl.f_bytes + pl.b_bytes);
   uint8_t* ws = nullptr;
   if (need > 0) {
@@ -302,8 +303,8 @@ cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, con
       ldf = pl.ldf;
     }
   }
-  const float* Bhat = nullptr;
-  if (algo == CGB_ALGO_EXPLICIT) {
+  const float* Bhat = Bext;
+  if (algo == CGB_ALGO_EXPLICIT && !Bext) {
     float* B = reinterpret_cast<float*>(ws + pl.f_bytes);
     if ((e = launch_im2col(I, B, pl.ldb, g, s)) != cudaSuccess) return cuda_fail(e, "im2col");
     Bhat = B;
@@ -330,6 +331,43 @@ cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, con
   }
   if (e != cudaSuccess) return cuda_fail(e, "conv kernel launch");
   return CGB_OK;
+}
+
+cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, const cgb_conv_params* cp, float* O,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (algo != CGB_ALGO_EXPLICIT && algo != CGB_ALGO_FUSED) return fail(CGB_INVALID_ARGUMENT, "unknown algo");
+  if (precision < CGB_PREC_AUTO || precision > CGB_PREC_FFMA)
+    return fail(CGB_INVALID_ARGUMENT, "unknown precision");
+  if (!F || !I || !O) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  if ((st = check_device_limits(g))) return st;
+  return conv_impl(algo, precision, F, I, g, O, workspace, workspace_bytes, stream, nullptr, 0);
+}
+
+// C (m x n) = A (m x k) * B (k x n), column-major: a 1x1 convolution over 1x1 images
+// (F = A as k_n=m x c_i=k, I = B as c_i=k x b=n, O = C), run as the explicit path
+// with B itself as the lowered matrix (the reference's fc layers, bench.cpp:140-153).
+cgb_status cgb_gemm(int precision, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                    int64_t m, int64_t n, int64_t k, void* workspace, size_t workspace_bytes, void* stream) {
+  if (m < 1 || n < 1 || k < 1) return fail(CGB_INVALID_GEOMETRY, "gemm dimensions must be positive");
+  if (lda != m || ldc != m || ldb < k)
+    return fail(CGB_DIMENSION_MISMATCH, "gemm needs lda == m, ldc == m and ldb >= k (dense column-major A and C)");
+  if (precision < CGB_PREC_AUTO || precision > CGB_PREC_FFMA)
+    return fail(CGB_INVALID_ARGUMENT, "unknown precision");
+  if (!A || !B || !C) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  cgb_conv_params cp{m, 1, 1, k, 1, 1, n, 1, 0};
+  ConvGeom g;
+  cgb_status st = make_geom(&cp, &g);
+  if (st) return st;
+  if ((st = check_device_limits(g))) return st;
+  // The explicit-path kernels read B in 16-byte vectors: an unaligned B (or ld) is
+  // lowered into an aligned, zero-padded copy first (im2col of a 1x1 conv is exactly that).
+  if (ldb % 4 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0)
+    return conv_impl(CGB_ALGO_EXPLICIT, precision, A, B, g, C, workspace, workspace_bytes, stream, B, ldb);
+  if (ldb != k) return fail(CGB_DIMENSION_MISMATCH, "gemm needs ldb == k or a multiple of 4 (16-byte aligned B)");
+  return conv_impl(CGB_ALGO_EXPLICIT, precision, A, B, g, C, workspace, workspace_bytes, stream, nullptr, 0);
 }
 
 cgb_status cgb_conv_gemm(const float* F, const float* I, const cgb_conv_params* cp, const cgb_blocking_params* bp,
