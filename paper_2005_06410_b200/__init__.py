@@ -38,7 +38,7 @@ __all__ = [
 ALGOS = {"explicit": 0, "im2col": 0, "fused": 1, "convgemm": 1}
 PRECISIONS = {"auto": 0, "3xtf32": 1, "tf32": 2, "ffma": 3}
 PATHS = {0: "none", 1: "tcgen05-implicit", 2: "tcgen05-explicit", 3: "ffma-implicit", 4: "ffma-explicit",
-         5: "tcgen05-shifted", 6: "tcgen05-gather"}
+         5: "tcgen05-shifted", 6: "tcgen05-gather", 7: "tcgen05-shifted-wim"}
 
 
 class InvalidGeometry(ValueError):

@@ -196,6 +196,13 @@ static int resolve_precision(int prec, const ConvGeom& g) {
   return g.k < 32 ? CGB_PREC_FFMA : CGB_PREC_3XTF32;
 }
 
+static bool use_wim(int algo, int prec, const ConvGeom& g) {
+  return algo == CGB_ALGO_FUSED && tf32_family(prec) && !shifted_supported(g) && wim_supported(g);
+}
+static int64_t wim_filter_bytes(int prec, const ConvGeom& g) {
+  return align_up(g.k_n * g.k_h * 32 * 4, 256) * (prec == CGB_PREC_3XTF32 ? 2 : 1);
+}
+
 static Plan make_plan(int algo, int prec, const ConvGeom& g, const float* F) {
   Plan pl{};
   pl.algo = algo;
@@ -254,8 +261,9 @@ cgb_status cgb_validate_blocking(const cgb_blocking_params* bp) {
 int64_t cgb_conv_workspace_bytes(int algo, int precision, const cgb_conv_params* cp) {
   ConvGeom g;
   if (make_geom(cp, &g)) return -1;
-  const Plan pl = make_plan(algo, resolve_precision(precision, g), g, nullptr);
-  return pl.f_bytes + pl.b_bytes;
+  const int prec = resolve_precision(precision, g);
+  const Plan pl = make_plan(algo, prec, g, nullptr);
+  return std::max<int64_t>(pl.f_bytes + pl.b_bytes, use_wim(algo, prec, g) ? wim_filter_bytes(prec, g) : 0);
 }
 
 // The operator body behind cgb_conv and cgb_gemm. Bext != NULL: the lowered matrix B
@@ -272,7 +280,9 @@ static cgb_status conv_impl(int algo, int precision, const float* F, const float
     pl.b_bytes = 0;
     pl.ldb = ldb_ext;
   }
-  const size_t need = (size_t)(pl.f_bytes + pl.b_bytes);
+  // low-channel layers (c_i < 16: the stem, VGG conv1) on the tensor cores: w-im2col mode
+  const bool wim = !Bext && use_wim(algo, prec, g);
+  const size_t need = std::max<size_t>((size_t)(pl.f_bytes + pl.b_bytes), wim ? (size_t)wim_filter_bytes(prec, g) : 0);
   uint8_t* ws = nullptr;
   if (need > 0) {
     if (workspace) {
@@ -290,6 +300,18 @@ static cgb_status conv_impl(int algo, int precision, const float* F, const float
   const float* f_hi = F;
   const float* f_lo = nullptr;
   int64_t ldf = g.k_n;
+  if (wim) {
+    float* hi = reinterpret_cast<float*>(ws);
+    float* lo = prec == CGB_PREC_3XTF32 ? reinterpret_cast<float*>(ws + wim_filter_bytes(prec, g) / 2) : nullptr;
+    if ((e = launch_wim_filter_prep(F, hi, lo, g, s)) != cudaSuccess) return cuda_fail(e, "wim filter_prep");
+    e = launch_tc_conv_wim(hi, lo, I, O, g, prec == CGB_PREC_3XTF32, s);
+    if (e == cudaSuccess) {
+      g_last_path = 7;
+      return CGB_OK;
+    }
+    if (e != cudaErrorNotSupported) return cuda_fail(e, "conv kernel launch");
+    // no fitting configuration: the generic kernels below (the workspace covers both)
+  }
   if (tf32_family(prec)) {
     if (pl.direct_filters) {
       f_hi = F;

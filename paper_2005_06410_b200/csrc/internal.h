@@ -62,6 +62,13 @@ cudaError_t launch_tc_gather(const float* f_hi, const float* f_lo, const float* 
 // V2: stride/phase "shifted window" tcgen05 kernel; returns cudaErrorNotSupported
 // when the geometry is outside its domain (caller falls back to launch_tc_conv).
 bool shifted_supported(const ConvGeom& g);
+// Low-channel mode of the shifted-window kernel ("w-im2col"): each window row holds the
+// k_w*c_i values of one output row's w-taps (k_w*c_i <= 32), only the k_h taps are row
+// shifts. For the stem and VGG conv1 (c_i = 3). Filters from launch_wim_filter_prep.
+bool wim_supported(const ConvGeom& g);
+cudaError_t launch_wim_filter_prep(const float* F, float* hi, float* lo, const ConvGeom& g, cudaStream_t st);
+cudaError_t launch_tc_conv_wim(const float* f_hi, const float* f_lo, const float* I, float* O, const ConvGeom& g,
+                               bool split, cudaStream_t st);
 cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t ldf, const float* I, float* O,
                                    const ConvGeom& g, bool split, cudaStream_t st);
 

@@ -71,6 +71,11 @@ struct Args {
   int32_t dp_tiles, sk_units, groups;
   int* counters;      // [sk tile][ranks*4 epilogue warps] pieces written; zero between launches
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
+  int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
+  int32_t wim;        // w-im2col mode: a row holds the k_w*c_i values of one output row's w-taps
+  int32_t wim_kw, wim_ci;  // the real k_w and c_i in that mode (k_w = 1 and c_i = 32 above)
+  int32_t wim_off[32];     // w-im2col element j = c + c_i*kw: c*plane + kw*h_i (constant bank, uniform)
+  int32_t wim_dw[32];      //   and its kw (a large negative value past k_w*c_i)
   unsigned long long* stats;  // per-CTA cycle counters when dbg & 64 (profiling only)
   int32_t dbg;        // profiling switches (CGB_DEBUG_SW): 1 = producers skip loads, 2 = skip MMAs,
                       //   4 = skip epilogue stores, 8 = skip filter TMA
@@ -259,6 +264,48 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     };
     int tile, cc0, cc1;
+    if (a.wim) {
+      // ---- w-im2col rows (low-channel layers): row (h-phase pha, hq, wo, image) holds
+      // I(s*hq + pha - p, s*wo + kw - p, c) at element j = c + c_i*kw (zero past k_w*c_i and
+      // in the padding); only the k_h taps are row shifts. One chunk per tile.
+      for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
+        const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
+        for (int cc = cc0; cc < cc1; ++cc, ++it) {
+          const int s = it % A_SLOTS;
+          const uint32_t ph = (it / A_SLOTS) & 1;
+          const uint32_t base_hi = smem_u32(a_slot(s, 0));
+          const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
+          mbar_wait_warp(&a_empty[s], ph ^ 1);
+          for (int u = warp; u < units && !(a.dbg & 1); u += PRODUCER_WARPS) {
+            const int32_t row = u * rows_per_unit + lane_row;
+            const int32_t Q = m0 + row;
+            const float* src = I;
+            int32_t w0 = -(1 << 20);
+            if (row < a.R && Q < a.Mp32) {
+              const int32_t bb = Q / hw_q;
+              const int32_t rem = Q - bb * hw_q;
+              const int32_t wo = rem / a.Hq, hq = rem - wo * a.Hq;
+              const int32_t h = a.s * hq + lane_pha - a.p;
+              if ((unsigned)h < (unsigned)a.h_i) {
+                w0 = a.s * wo - a.p;
+                src = I + (int64_t)bb * a.wim_ci * a.plane + (int64_t)w0 * a.h_i + h;
+              }
+            }
+            float v[BK];
+#pragma unroll
+            for (int e = 0; e < BK; ++e) {
+              // elements past ksteps*8 are never read by the MMAs: no loads for them
+              const int32_t w = w0 + a.wim_dw[e];
+              v[e] = (e < a.ksteps * 8 && (unsigned)w < (unsigned)a.w_i) ? ldg_stream(src + a.wim_off[e]) : 0.0f;
+            }
+            store_rows(row, v, base_hi + (uint32_t)lane_pha * slot_stride, base_lo + (uint32_t)lane_pha * slot_stride);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(PAIR ? &a_ready[s] : &a_full[s]);
+        }
+      }
+    } else
     for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
       const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
       for (int cc = cc0; cc < cc1; ++cc, ++it) {
@@ -417,6 +464,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (!(a.dbg & 2)) {
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk)
+                if (kk < a.ksteps)
 #pragma unroll
                 for (int hf = 0; hf < BN / C::UMMA_N; ++hf)
 #pragma unroll
@@ -741,6 +789,8 @@ static Args make_args(const ConvGeom& g) {
   a.Mp32 = (int32_t)a.Mp;
   a.plane = g.h_i * g.w_i;
   a.R = 0; a.m_tiles = 0; a.n_tiles = 0;
+  a.ksteps = BK / 8;
+  a.wim = 0; a.wim_kw = 1; a.wim_ci = a.c_i;
   const char* dbg = getenv("CGB_DEBUG_SW");
   a.dbg = dbg ? atoi(dbg) : 0;
   a.stats = nullptr;
@@ -953,6 +1003,56 @@ cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  return sw::dispatch(th, tl, I, O, a, split, sms, st);
+}
+
+bool wim_supported(const ConvGeom& g) {
+  if (g.s > 2 || g.k_n % 4 != 0 || g.k_w * g.c_i > 32 || g.k_h > 64) return false;
+  const int64_t hq = sw::plane_period(g.h_i, g.h_o, g.k_h, g.s, g.p);
+  if ((double)hq / (double)g.h_o > 1.7) return false;
+  return hq * g.w_o * g.b < (int64_t(1) << 30) && g.c_i * g.h_i * g.w_i * g.b < (int64_t(1) << 31);
+}
+
+// w-im2col mode: the kernel sees a (k_h x 1) convolution over 32 "channels" (one chunk)
+// whose window rows the producers build from the k_w*c_i real (kw, c) values; filters
+// come from launch_wim_filter_prep as a (k_n, k_h, 32) tap-major array.
+cudaError_t launch_tc_conv_wim(const float* f_hi, const float* f_lo, const float* I, float* O, const ConvGeom& g,
+                               bool split, cudaStream_t st) {
+  sw::Args a = sw::make_args(g);
+  a.wim = 1;
+  a.wim_kw = (int32_t)g.k_w;
+  a.wim_ci = (int32_t)g.c_i;
+  a.k_w = 1;
+  a.c_i = sw::BK;
+  a.CC = 1;
+  a.taps = a.k_h;
+  a.nph_w = 1;
+  a.NPH = a.nph_h;
+  a.Wq = a.w_o;
+  a.dmax = (a.k_h - 1) / a.s;
+  a.Mp = (int64_t)a.Hq * a.Wq * g.b;
+  a.Mp32 = (int32_t)a.Mp;
+  a.ksteps = (int32_t)((g.k_w * g.c_i + 7) / 8);
+  for (int j = 0; j < sw::BK; ++j) {
+    const int kw = j / (int)g.c_i, c = j - kw * (int)g.c_i;
+    a.wim_off[j] = (int32_t)(c * g.h_i * g.w_i + kw * g.h_i);
+    a.wim_dw[j] = kw < g.k_w ? kw : -(1 << 20);
+  }
+  a.vec = (g.k_n % 8) == 0 && reinterpret_cast<uintptr_t>(O) % 32 == 0;
+  ConvGeom gf = g;  // the prepared filters: k_h taps of 32 channels
+  gf.k_w = 1;
+  gf.c_i = sw::BK;
+  CUtensorMap th, tl;
+  cudaError_t e = make_filter_tmap_tapmajor(&th, f_hi, gf);
+  if (e != cudaSuccess) return e;
+  if (split) {
+    if ((e = make_filter_tmap_tapmajor(&tl, f_lo, gf)) != cudaSuccess) return e;
+  } else {
+    tl = th;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return sw::dispatch(th, tl, I, O, a, split, sms, st);
 }
 

@@ -256,4 +256,35 @@ cudaError_t launch_filter_prep(const float* F, float* hi, float* lo, int64_t ldf
   return cudaGetLastError();
 }
 
+// w-im2col filters for the low-channel shifted-window mode: F'(n, kh, j) with
+// j = c + c_i*kw (< k_w*c_i <= 32), zero for j >= k_w*c_i, as a (k_n, k_h, 32) array
+// (the tap-major TMA map with k_h taps of 32 channels). 3xTF32: hi/lo split.
+__global__ void __launch_bounds__(256) wim_filter_prep_kernel(const float* __restrict__ F, float* __restrict__ hi,
+                                                              float* __restrict__ lo, int64_t k_n, int64_t k_h,
+                                                              int64_t k_w, int64_t c_i) {
+  const int64_t total = k_n * k_h * 32;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = idx % k_n, kh = (idx / k_n) % k_h, j = idx / (k_n * k_h);
+    const int64_t kw = j / c_i, c = j - kw * c_i;
+    const float f = kw < k_w ? __ldg(F + n + k_n * (kh + k_h * (kw + k_w * c))) : 0.0f;
+    if (lo) {
+      const float h = to_tf32(f);
+      hi[idx] = h;
+      lo[idx] = to_tf32(f - h);
+    } else {
+      hi[idx] = f;
+    }
+  }
+}
+
+cudaError_t launch_wim_filter_prep(const float* F, float* hi, float* lo, const ConvGeom& g, cudaStream_t st) {
+  const int64_t total = g.k_n * g.k_h * 32;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 8);
+  wim_filter_prep_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(F, hi, lo, g.k_n, g.k_h, g.k_w,
+                                                                                 g.c_i);
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace cgb

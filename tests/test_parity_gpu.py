@@ -285,6 +285,12 @@ VARIANT_CASES = [
     # pad > k-1 and asymmetric periods: wrapped reads land in shared zero rows
     (dict(k_n=64, k_h=3, k_w=2, c_i=32, h_i=11, w_i=9, b=3, s=1, p=2), "tcgen05-shifted"),
     (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=20, w_i=20, b=2, s=3, p=1), "tcgen05-gather"),
+    # low-channel layers: w-im2col rows (k_w*c_i <= 32 values per row), k_h taps as shifts
+    (dict(k_n=64, k_h=7, k_w=7, c_i=3, h_i=40, w_i=40, b=2, s=2, p=3), "tcgen05-shifted-wim"),
+    (dict(k_n=64, k_h=3, k_w=3, c_i=3, h_i=30, w_i=30, b=2, s=1, p=1), "tcgen05-shifted-wim"),
+    (dict(k_n=32, k_h=3, k_w=3, c_i=1, h_i=17, w_i=13, b=3, s=1, p=0), "tcgen05-shifted-wim"),
+    (dict(k_n=48, k_h=4, k_w=4, c_i=8, h_i=12, w_i=12, b=2, s=2, p=1), "tcgen05-shifted-wim"),
+    (dict(k_n=96, k_h=5, k_w=3, c_i=5, h_i=20, w_i=16, b=2, s=1, p=2), "tcgen05-shifted-wim"),
 ]
 
 
