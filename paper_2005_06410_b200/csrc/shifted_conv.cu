@@ -846,8 +846,8 @@ static const Cand kCands[] = {
     {2, 64, 0, 1, 8, 1, 1},  {1, 64, 0, 1, 8, 1, 1},  {2, 128, 0, 1, 4, 1, 1}, {1, 128, 0, 1, 4, 1, 1},
     {1, 256, 0, 1, 3, 1, 1},
     // deep filter rings: only for filter-stream-heavy layers (BN = 256 and >= 2 filter
-    // tiles, e.g. 7x7/14x14 512->512: 3-9% faster); elsewhere the extra shared memory
-    // costs L1 and measured slower (dispatch)
+    // tiles or a stride-1 window, e.g. 7x7/14x14 512->512, 14x14 256->256: 3-9% faster);
+    // elsewhere the extra shared memory costs L1 and measured slower (dispatch)
     {1, 256, 0, 2, 9, 1, 1}, {1, 256, 0, 2, 4, 1, 1},
     // two window units in flight per producer warp: staging-bound layers only (BN = 64,
     // or stride 2 with BN <= 128: 56x56 64->64 3% and 56->28 128 8% faster; slower where
@@ -950,7 +950,10 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
       }
     }
     if (const char* f = getenv("CGB_SW_MT")) mt_max = atoi(f);  // profiling override
-    const bool deep_first = bn == 256 && n_tiles >= 2;
+    // deep filter rings for the filter-stream-heavy layers: BN = 256 with several filter
+    // tiles, or with a stride-1 (small) window that leaves the shared memory for them
+    // (14x14 256->256: 62 -> 57 us); stride-2 windows keep the L1 instead
+    const bool deep_first = bn == 256 && (n_tiles >= 2 || a.s == 1);
     // staging-bound layers (stride-2 windows with BN <= 128, or BN = 64) first try the
     // candidates with two units in flight per producer warp
     const bool upi2 = (a.s == 2 && bn <= 128) || bn == 64;
