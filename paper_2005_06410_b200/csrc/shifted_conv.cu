@@ -857,6 +857,7 @@ static const Cand kCands[] = {
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
 constexpr int kFirstUpi2Cand = 38;
+constexpr int kFirstProbeCand = 42;  // candidates from here on are CGB_SW_CFG probes only
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st) {
@@ -957,8 +958,8 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     // staging-bound layers (stride-2 windows with BN <= 128, or BN = 64) first try the
     // candidates with two units in flight per producer warp
     const bool upi2 = (a.s == 2 && bn <= 128) || bn == 64;
-    const int nupi2 = kNumCands - kFirstUpi2Cand;
-    for (int k = 0; k < kNumCands + nupi2; ++k) {
+    const int nupi2 = kFirstProbeCand - kFirstUpi2Cand;
+    for (int k = 0; k < kFirstUpi2Cand + nupi2; ++k) {
       int i;
       if (k < nupi2) {
         if (!upi2) continue;
