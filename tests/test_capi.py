@@ -75,3 +75,26 @@ def test_blocking_validation():
 def test_version_and_counters():
     assert b"sm_100a" in _lib.lib.cgb_version()
     assert cg.kernel_launch_count() >= 0
+
+
+def test_gemm_argument_errors():
+    """cgb_gemm validates before touching the device (gemm.hpp:51-53 DimensionMismatch)."""
+    L = _lib.lib
+    # non-positive dimensions -> InvalidGeometry
+    assert L.cgb_gemm(0, 1, 4, 1, 4, 1, 4, 0, 4, 4, None, 0, None) == 1
+    # lda != m, ldc != m, ldb < k -> DimensionMismatch
+    assert L.cgb_gemm(0, 1, 8, 1, 4, 1, 4, 4, 4, 4, None, 0, None) == 2
+    assert L.cgb_gemm(0, 1, 4, 1, 4, 1, 8, 4, 4, 4, None, 0, None) == 2
+    assert L.cgb_gemm(0, 1, 4, 1, 3, 1, 4, 4, 4, 4, None, 0, None) == 2
+    assert b"ld" in L.cgb_last_error()
+    # unknown precision, null pointers -> InvalidArgument
+    assert L.cgb_gemm(9, 1, 4, 1, 4, 1, 4, 4, 4, 4, None, 0, None) == 4
+    assert L.cgb_gemm(0, None, 4, 1, 4, 1, 4, 4, 4, 4, None, 0, None) == 4
+
+
+def test_low_channel_workspace():
+    """The stem (c_i = 3) takes the w-im2col filter array (k_n x k_h x 32, hi/lo in
+    3xTF32) as its fused-path workspace."""
+    stem = (64, 7, 7, 3, 224, 224, 256, 2, 3)
+    assert cg.conv_workspace_bytes(stem, "fused", "tf32") >= 64 * 7 * 32 * 4
+    assert cg.conv_workspace_bytes(stem, "fused", "3xtf32") >= 2 * 64 * 7 * 32 * 4
