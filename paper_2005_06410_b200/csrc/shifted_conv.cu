@@ -72,6 +72,7 @@ struct Args {
   int* counters;      // [sk tile][ranks*4 epilogue warps] pieces written; zero between launches
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
+  int32_t pstore;     // epilogue stores: 1 lane pairs 64 B (default), 0 per-lane 32 B (CGB_SW_PSTORE=0)
   int32_t wim;        // w-im2col mode: a row holds the k_w*c_i values of one output row's w-taps
   int32_t wim_kw, wim_ci;  // the real k_w and c_i in that mode (k_w = 1 and c_i = 32 above)
   int32_t wim_off[32];     // w-im2col element j = c + c_i*kw: c*plane + kw*h_i (constant bank, uniform)
@@ -567,25 +568,48 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const uint32_t trow = tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS + mt * BN;
 #pragma unroll 1
-        for (int cb = 0; cb < BN / 64; ++cb) {
-          uint32_t r[64];
-          tmem_ld_32x32b_x32(trow + cb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-          tmem_ld_32x32b_x32(trow + cb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        for (int cb = 0; cb < BN / 32; ++cb) {  // 32-column blocks: 32 live data registers
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(trow + cb * 32, r);
           tmem_ld_wait();
-          const int nb = n0 + cb * 64;
-          if (P >= 0 && !(a.dbg & 4)) {
+          const int nb = n0 + cb * 32;
+          if (a.pstore && a.vec && nb + 32 <= a.k_n && !add && !(a.dbg & 4)) {
+            // Lane pairs write whole 64-byte runs: in store A_k the pair writes segments
+            // 2k, 2k+1 (8 floats each) of the even lane's pixel, in B_k those of the odd
+            // lane's pixel, after one shfl.xor exchange. Each warp store then touches 16
+            // lines with 64 bytes each instead of 32 lines with 32 bytes: half the L1->L2
+            // write requests, which bound the epilogue (~1 request per clock per SM).
+            // (Lane quads writing whole 128-byte lines after a 4x4 shuffle transpose
+            // measured slower: the extra shuffles and selects cost more than they save.)
+            const int par = lane & 1;
+            const int64_t PA = __shfl_sync(0xffffffffu, P, lane & ~1), PB = __shfl_sync(0xffffffffu, P, lane | 1);
+            float* dA = O + PA * a.k_n + nb + 8 * par;
+            float* dB = O + PB * a.k_n + nb + 8 * par;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              uint32_t x[8], v[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) x[i] = __shfl_xor_sync(0xffffffffu, par ? r[16 * k + i] : r[16 * k + 8 + i], 1);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = par ? x[i] : r[16 * k + i];
+              if (PA >= 0) st_global_v8(dA + 16 * k, v);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = par ? r[16 * k + 8 + i] : x[i];
+              if (PB >= 0) st_global_v8(dB + 16 * k, v);
+            }
+          } else if (P >= 0 && !(a.dbg & 4)) {
             float* dst = O + P * a.k_n + nb;
-            if (a.vec && nb + 64 <= a.k_n) {
+            if (a.vec && nb + 32 <= a.k_n) {
               if (!add) {
 #pragma unroll
-                for (int j = 0; j < 64; j += 8) st_global_v8(dst + j, &r[j]);
+                for (int j = 0; j < 32; j += 8) st_global_v8(dst + j, &r[j]);
               } else {
 #pragma unroll
-                for (int j = 0; j < 64; j += 4) red_add_v4(dst + j, &r[j]);
+                for (int j = 0; j < 32; j += 4) red_add_v4(dst + j, &r[j]);
               }
             } else {
 #pragma unroll
-              for (int j = 0; j < 64; ++j)
+              for (int j = 0; j < 32; ++j)
                 if (nb + j < a.k_n) {
                   if (!add) dst[j] = __uint_as_float(r[j]);
                   else atomicAdd(dst + j, __uint_as_float(r[j]));
@@ -790,6 +814,8 @@ static Args make_args(const ConvGeom& g) {
   a.plane = g.h_i * g.w_i;
   a.R = 0; a.m_tiles = 0; a.n_tiles = 0;
   a.ksteps = BK / 8;
+  const char* ps = getenv("CGB_SW_PSTORE");
+  a.pstore = ps ? atoi(ps) : 1;
   a.wim = 0; a.wim_kw = 1; a.wim_ci = a.c_i;
   const char* dbg = getenv("CGB_DEBUG_SW");
   a.dbg = dbg ? atoi(dbg) : 0;
