@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_ld_32x32b_x32(trow + cb * 32, r);
           tmem_ld_wait();
           const int nb = n0 + cb * 32;
-          if (a.pstore && a.vec && nb + 32 <= a.k_n && !add && !(a.dbg & 4)) {
+          if (a.pstore && a.vec && nb + 32 <= a.k_n && !(a.dbg & 4)) {
             // Lane pairs write whole 64-byte runs: in store A_k the pair writes segments
             // 2k, 2k+1 (8 floats each) of the even lane's pixel, in B_k those of the odd
             // lane's pixel, after one shfl.xor exchange. Each warp store then touches 16
@@ -592,10 +592,22 @@ __global__ void __launch_bounds__(THREADS, 1)
               for (int i = 0; i < 8; ++i) x[i] = __shfl_xor_sync(0xffffffffu, par ? r[16 * k + i] : r[16 * k + 8 + i], 1);
 #pragma unroll
               for (int i = 0; i < 8; ++i) v[i] = par ? x[i] : r[16 * k + i];
-              if (PA >= 0) st_global_v8(dA + 16 * k, v);
+              if (PA >= 0) {
+                if (!add) st_global_v8(dA + 16 * k, v);
+                else {  // stream-K piece: the pair's 16-byte reds share 128-byte lines too
+                  red_add_v4(dA + 16 * k, v);
+                  red_add_v4(dA + 16 * k + 4, v + 4);
+                }
+              }
 #pragma unroll
               for (int i = 0; i < 8; ++i) v[i] = par ? r[16 * k + 8 + i] : x[i];
-              if (PB >= 0) st_global_v8(dB + 16 * k, v);
+              if (PB >= 0) {
+                if (!add) st_global_v8(dB + 16 * k, v);
+                else {
+                  red_add_v4(dB + 16 * k, v);
+                  red_add_v4(dB + 16 * k + 4, v + 4);
+                }
+              }
             }
           } else if (P >= 0 && !(a.dbg & 4)) {
             float* dst = O + P * a.k_n + nb;
