@@ -69,6 +69,10 @@ struct Args {
   // contiguous, balanced range per group (stream-K), then dp_tiles whole tiles
   // round-robin over the `groups` CTAs (pairs: clusters).
   int32_t dp_tiles, sk_units, groups;
+  // Tail tiles: m-tiles [m_full, m_tiles) have tail_mt (< MT) subtiles, so the last round
+  // of a layer whose row count leaves it half empty is cut into smaller tiles that fill
+  // all groups (0 = every m-tile has MT subtiles).
+  int32_t m_full, tail_mt;
   int* counters;      // [sk tile][ranks*4 epilogue warps] pieces written; zero between launches
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
@@ -116,6 +120,21 @@ CGB_DEV int sk_group_of(const Args& a, int x) {
   int c = (int)((int64_t)x * a.groups / a.sk_units);
   while (c + 1 < a.groups && sk_begin(a, c + 1) <= x) ++c;
   return c;
+}
+
+// First padded row of this CTA's part of a tile and its subtile count (MT, or tail_mt for
+// the tail m-tiles); pair tiles stack rank 0's and rank 1's rows.
+template <int MT, bool PAIR>
+CGB_DEV void tile_rows(const Args& a, int tile, uint32_t rank, int32_t& m0, int& mtc) {
+  constexpr int P = PAIR ? 2 : 1;
+  const int32_t mi = tile % a.m_tiles;
+  if (a.tail_mt && mi >= a.m_full) {
+    mtc = a.tail_mt;
+    m0 = a.m_full * (P * MT * 128) + (mi - a.m_full) * (P * a.tail_mt * 128) + (int32_t)rank * a.tail_mt * 128;
+  } else {
+    mtc = MT;
+    m0 = mi * (P * MT * 128) + (int32_t)rank * (MT * 128);
+  }
 }
 
 template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR = false>
@@ -170,7 +189,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   // [m0 + rank*MT*128, +MT*128) of the pair tile and filters [n0 + rank*BN/2, +BN/2) of B.
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const int gid = PAIR ? (int)cluster_id_x() : (int)blockIdx.x;  // work group (CTA or CTA pair)
-  constexpr int PAIR_ROWS = (PAIR ? 2 : 1) * MT * 128;
 
   if (warp == TMA_WARP) {
     if (lane == 0) {
@@ -221,8 +239,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     // parities) -> one 128-byte line per channel; every 8-lane group stores 8 consecutive
     // rows of one phase -> conflict-free 16-byte shared stores under the 128B swizzle.
     const int rows_per_unit = 32 / a.nph_h;
-    const int row_blocks = (a.R + rows_per_unit - 1) / rows_per_unit;
-    const int units = a.nph_w * row_blocks;
+    int32_t Rt = a.R;  // staged rows of the current tile (fewer for tail tiles)
+    int row_blocks = (Rt + rows_per_unit - 1) / rows_per_unit;
+    int units = a.nph_w * row_blocks;
+    auto set_tile_rows = [&](int mtc) {
+      Rt = mtc * 128 + a.dmax;
+      row_blocks = (Rt + rows_per_unit - 1) / rows_per_unit;
+      units = a.nph_w * row_blocks;
+    };
     const int32_t hw_q = a.Hq * a.Wq;
     const int32_t plane = (int32_t)a.plane;
     const int lane_row = (lane & 7) + 8 * (lane / (8 * a.nph_h));
@@ -231,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int it = 0;  // chunk counter across tiles (slot ring position)
     auto row_src = [&](int32_t row, int32_t ph_a, int32_t ph_c, int32_t m0, int cc, bool& ok) -> const float* {
       const int32_t Q = m0 + row;
-      ok = row < a.R && Q < a.Mp32;
+      ok = row < Rt && Q < a.Mp32;
       if (!ok) return I;
       const int32_t bb = Q / hw_q;
       const int32_t rem = Q - bb * hw_q;
@@ -250,7 +274,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     };
     auto store_rows = [&](int32_t row, const float (&v)[BK], uint32_t dst_hi, uint32_t dst_lo) {
-      if (row >= a.R) return;
+      if (row >= Rt) return;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const uint32_t off = row * 128 + ((ch ^ (row & 7)) << 4);
@@ -270,7 +294,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       // I(s*hq + pha - p, s*wo + kw - p, c) at element j = c + c_i*kw (zero past k_w*c_i and
       // in the padding); only the k_h taps are row shifts. One chunk per tile.
       for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
-        const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
+        int32_t m0;
+        int mtc;
+        tile_rows<MT, PAIR>(a, tile, rank, m0, mtc);
+        set_tile_rows(mtc);
         for (int cc = cc0; cc < cc1; ++cc, ++it) {
           const int s = it % A_SLOTS;
           const uint32_t ph = (it / A_SLOTS) & 1;
@@ -282,7 +309,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int32_t Q = m0 + row;
             const float* src = I;
             int32_t w0 = -(1 << 20);
-            if (row < a.R && Q < a.Mp32) {
+            if (row < Rt && Q < a.Mp32) {
               const int32_t bb = Q / hw_q;
               const int32_t rem = Q - bb * hw_q;
               const int32_t wo = rem / a.Hq, hq = rem - wo * a.Hq;
@@ -308,7 +335,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     } else
     for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
-      const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
+      int32_t m0;
+      int mtc;
+      tile_rows<MT, PAIR>(a, tile, rank, m0, mtc);
+      set_tile_rows(mtc);
       for (int cc = cc0; cc < cc1; ++cc, ++it) {
         const int s = it % A_SLOTS;
         const uint32_t ph = (it / A_SLOTS) & 1;
@@ -436,6 +466,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (; seg_get(a, gid, t, tile, cc0, cc1); ++t) {
         const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
         const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
+        int32_t m0u;
+        int mtc;
+        tile_rows<MT, PAIR>(a, tile, 0, m0u, mtc);
         unsigned long long c0 = st ? clock64() : 0;
         if (PAIR) mbar_wait_spin_cl(&t_empty[acc_set], acc_ph ^ 1);
         else mbar_wait_spin(&t_empty[acc_set], acc_ph ^ 1);
@@ -470,6 +503,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int hf = 0; hf < BN / C::UMMA_N; ++hf)
 #pragma unroll
                   for (int mt = 0; mt < MT; ++mt) {
+                    if (mt >= mtc) break;  // tail tile: fewer M subtiles
                     const uint64_t ad = at + (uint64_t)(mt * 1024 + kk * 2);
                     const uint64_t bd = bt + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
                     const uint32_t d = d_base + mt * BN + hf * C::UMMA_N;
@@ -520,7 +554,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (; seg_get(a, gid, t, tile, cc0, cc1); ++t) {
       const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
       const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
-      const int32_t m0 = (tile % a.m_tiles) * PAIR_ROWS + (int32_t)rank * (MT * 128);
+      int32_t m0;
+      int mtc;
+      tile_rows<MT, PAIR>(a, tile, rank, m0, mtc);
       const int n0 = (tile / a.m_tiles) * BN;
       unsigned long long e0 = (a.dbg & 64) ? clock64() : 0;
       if (PAIR) {
@@ -557,7 +593,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
       }
 #pragma unroll 1
-      for (int mt = 0; mt < MT && !(a.dbg & 16); ++mt) {
+      for (int mt = 0; mt < mtc && !(a.dbg & 16); ++mt) {
         const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
         int64_t P = -1;
         if (Q < a.Mp32) {
@@ -723,16 +759,43 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   if (const char* pad = getenv("CGB_SW_SMEM_PAD"))  // profiling: shrink the L1 carve-out
     smem = std::max<size_t>(smem, (size_t)atoi(pad) * 1024);
   auto kern = sw_conv_kernel<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR, UPI>;
-  if (getenv("CGB_SW_VERBOSE"))
-    fprintf(stderr, "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d smem=%.1fKB\n", MT, BN,
-            (int)SPLIT, A_SLOTS, B_STAGES, (int)PAIR, UPI, smem / 1024.0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = a.m_tiles * a.n_tiles;
   const int gmax = PAIR ? sms / 2 : sms;
+  // Tail tiles (one filter tile, MT >= 2): when the whole-tile rounds leave a last round
+  // that smaller tiles of tail_mt subtiles fill in ONE round, cut it that way (56x56
+  // 64->64: 5 rounds of 1024-row pair tiles + 1 round of 512-row tiles instead of 6
+  // rounds, the last half empty). Relative tile times as in the dispatcher's cost model.
+  a.m_full = 0;
+  a.tail_mt = 0;
+  const char* te = getenv("CGB_SW_TAIL");  // 0 = never, 2 = whenever it fits (tests), default: by cost
+  const int tail_mode = te ? atoi(te) : 1;
+  if (a.n_tiles == 1 && MT >= 2 && tail_mode != 0) {
+    auto tt = [](int mt) { return mt >= 4 ? 1.8 * mt / 4 : (mt == 2 ? 1.0 : 0.62); };
+    const int64_t full_fit = a.Mp / pair_rows;
+    const int rounds_full = (int)(full_fit / gmax);
+    const int64_t rem = a.Mp - (int64_t)rounds_full * gmax * pair_rows;
+    const double t_plain = (double)((a.m_tiles + gmax - 1) / gmax) * tt(MT);
+    if (rounds_full >= 1 && rem > 0) {
+      for (int tmt = MT / 2; tmt >= 1; tmt /= 2) {
+        const int64_t tail_rows = (int64_t)(PAIR ? 2 : 1) * tmt * 128;
+        const int64_t n_tail = (rem + tail_rows - 1) / tail_rows;
+        if (n_tail > gmax) break;
+        // only where stream-K would not take the last round (fill >= kSkFill)
+        const double fill0 = (double)a.m_tiles / ((double)((a.m_tiles + gmax - 1) / gmax) * gmax);
+        if (tail_mode == 2 || (fill0 >= kSkFill && rounds_full * tt(MT) + tt(tmt) < 0.97 * t_plain)) {
+          a.m_full = rounds_full * gmax;
+          a.tail_mt = tmt;
+          a.m_tiles = (int32_t)(a.m_full + n_tail);
+        }
+        break;
+      }
+    }
+  }
+  const int tiles = a.m_tiles * a.n_tiles;
   // Work split: whole tiles round-robin while the last round is well filled; otherwise
   // the last one-to-two rounds of tiles are split by channel chunk over all groups
   // (stream-K), which needs the arrival counters.
@@ -747,7 +810,7 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   // split tile adds a red.add pass over its rows (L2 atomics), which measured slower than
   // the idle SMs it saves when ALL tiles would be split (1-round layers: 7x7, 14x14).
   // The fixup itself handles any number of pieces per tile (sk_mode 2 forces it).
-  const bool sk_ok = sk_mode == 2 ? (int64_t)tiles * a.CC >= 2 * gmax : tiles >= gmax;
+  const bool sk_ok = !a.tail_mt && (sk_mode == 2 ? (int64_t)tiles * a.CC >= 2 * gmax : tiles >= gmax);
   if (sk_mode != 0 && a.CC >= 2 && sk_ok && (fill < kSkFill || sk_mode == 2)) {
     const int dp = std::max(0, tiles / gmax - 1) * gmax;
     const int sk_tiles = tiles - dp;
@@ -757,6 +820,12 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
       a.sk_units = sk_tiles * a.CC;
     }
   }
+  if (getenv("CGB_SW_VERBOSE"))
+    fprintf(stderr,
+            "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d smem=%.1fKB tiles=%d (tail %d of mt %d) "
+            "sk_units=%d\n",
+            MT, BN, (int)SPLIT, A_SLOTS, B_STAGES, (int)PAIR, UPI, smem / 1024.0, tiles,
+            a.tail_mt ? a.m_tiles - a.m_full : 0, a.tail_mt, a.sk_units);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((PAIR ? 2 : 1) * a.groups));
   cfg.blockDim = dim3(THREADS);
@@ -825,6 +894,7 @@ static Args make_args(const ConvGeom& g) {
   a.Mp32 = (int32_t)a.Mp;
   a.plane = g.h_i * g.w_i;
   a.R = 0; a.m_tiles = 0; a.n_tiles = 0;
+  a.m_full = 0; a.tail_mt = 0;
   a.ksteps = BK / 8;
   const char* ps = getenv("CGB_SW_PSTORE");
   a.pstore = ps ? atoi(ps) : 1;
@@ -953,7 +1023,8 @@ static int bn_for(int k_n) { return k_n <= 64 ? 64 : (k_n <= 128 ? 128 : 256); }
 
 static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, const Args& a,
                             bool split, int sms, cudaStream_t st) {
-  const int bn = bn_for(a.k_n);
+  int bn = bn_for(a.k_n);
+  if (const char* f = getenv("CGB_SW_BN")) bn = atoi(f);  // profiling override: 64, 128 or 256
   const int n_tiles = (a.k_n + bn - 1) / bn;
   if (const char* f = getenv("CGB_SW_CFG")) {  // profiling override: force one candidate
     const int i = atoi(f);

@@ -346,6 +346,35 @@ def test_stream_k(orc, monkeypatch, case, prec):
         assert not np.array_equal(a, whole)
 
 
+# ---------------------------------------------------------------- tail tiles
+TAIL_CASES = [
+    # forced (CGB_SW_TAIL=2): whole 4-subtile pair tiles for one round, then 2-subtile
+    # (or 1-subtile) tail tiles for the remaining rows
+    dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=56, w_i=56, b=26, s=1, p=1),
+    dict(k_n=128, k_h=3, k_w=3, c_i=32, h_i=28, w_i=28, b=70, s=1, p=1),
+    dict(k_n=64, k_h=3, k_w=3, c_i=48, h_i=57, w_i=30, b=44, s=2, p=1),
+]
+
+
+@pytest.mark.parametrize("case", range(len(TAIL_CASES)))
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_tail_tiles(orc, monkeypatch, case, prec):
+    cp = TAIL_CASES[case]
+    F, I = rand_inputs(cp, 500 + case)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    dF, dI = to_dev(F), to_dev(I)
+    monkeypatch.setenv("CGB_SW_TAIL", "2")
+    a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    assert per_output_error(a, ref, scale) <= TOL[prec]
+    monkeypatch.setenv("CGB_SW_TAIL", "0")
+    b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    assert per_output_error(b, ref, scale) <= TOL[prec]
+    if cg.last_path() == "tcgen05-shifted":
+        # whole tiles in both launches (no stream-K split): the same bits either way
+        assert np.array_equal(a, b)
+
+
 def _offset_tensor4(a, shift):
     """CUDA leftmost-fastest tensor holding a, starting `shift` floats into its buffer
     (a user pointer that is only 4-byte aligned)."""
