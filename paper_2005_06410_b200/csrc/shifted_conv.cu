@@ -961,11 +961,15 @@ static const Cand kCands[] = {
     // or stride 2 with BN <= 128: 56x56 64->64 3% and 56->28 128 8% faster; slower where
     // the MMA or the filter stream binds)
     {4, 64, 0, 2, 8, 1, 2}, {2, 64, 0, 2, 8, 1, 2}, {1, 128, 0, 2, 4, 1, 2}, {2, 128, 0, 2, 6, 1, 2},
+    // 3xTF32 with a double-buffered (hi + lo) window: fits the stride-1 windows
+    {2, 64, 1, 2, 4, 1, 1}, {1, 64, 1, 2, 6, 1, 1}, {2, 128, 1, 2, 3, 1, 1}, {1, 128, 1, 2, 4, 1, 1},
+    {1, 256, 1, 2, 2, 1, 1},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
 constexpr int kFirstUpi2Cand = 38;
-constexpr int kFirstProbeCand = 42;  // candidates from here on are CGB_SW_CFG probes only
+constexpr int kFirstSplit2Cand = 42;  // 3xTF32 with two window slots
+constexpr int kFirstProbeCand = 47;  // candidates from here on are CGB_SW_CFG probes only
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st) {
@@ -1014,6 +1018,11 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(39, 2, 64, false, 2, 8, true, 2)
     CGB_SW_CASE(40, 1, 128, false, 2, 4, true, 2)
     CGB_SW_CASE(41, 2, 128, false, 2, 6, true, 2)
+    CGB_SW_CASE(42, 2, 64, true, 2, 4, true, 1)
+    CGB_SW_CASE(43, 1, 64, true, 2, 6, true, 1)
+    CGB_SW_CASE(44, 2, 128, true, 2, 3, true, 1)
+    CGB_SW_CASE(45, 1, 128, true, 2, 4, true, 1)
+    CGB_SW_CASE(46, 1, 256, true, 2, 2, true, 1)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -1067,20 +1076,19 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     // staging-bound layers (stride-2 windows with BN <= 128, or BN = 64) first try the
     // candidates with two units in flight per producer warp
     const bool upi2 = (a.s == 2 && bn <= 128) || bn == 64;
-    const int nupi2 = kFirstProbeCand - kFirstUpi2Cand;
-    for (int k = 0; k < kFirstUpi2Cand + nupi2; ++k) {
-      int i;
-      if (k < nupi2) {
-        if (!upi2) continue;
-        i = kFirstUpi2Cand + k;
-      } else {
-        const int k2 = k - nupi2;
-        if (k2 >= kFirstUpi2Cand) break;
-        // deep-ring candidates first for filter-heavy layers, never otherwise
-        i = deep_first ? (k2 < kFirstUpi2Cand - kFirstDeepCand ? kFirstDeepCand + k2 : k2 - (kFirstUpi2Cand - kFirstDeepCand))
-                       : k2;
-        if (!deep_first && i >= kFirstDeepCand) continue;
-      }
+    // try order: 3xTF32 double-buffered windows (split), two-unit producers (upi2), deep
+    // filter rings (deep_first), then the regular table; probes never
+    int order[kFirstProbeCand];
+    int no = 0;
+    if (split)
+      for (int i = kFirstSplit2Cand; i < kFirstProbeCand; ++i) order[no++] = i;
+    if (upi2)
+      for (int i = kFirstUpi2Cand; i < kFirstSplit2Cand; ++i) order[no++] = i;
+    if (deep_first)
+      for (int i = kFirstDeepCand; i < kFirstUpi2Cand; ++i) order[no++] = i;
+    for (int i = 0; i < kFirstDeepCand; ++i) order[no++] = i;
+    for (int k = 0; k < no; ++k) {
+      const int i = order[k];
       const Cand& c = kCands[i];
       if (c.bn != bn || c.split != (int)split || c.mt > mt_max || c.pair != want_pair) continue;
       if (pass % 2 == 0 && c.as != 2) continue;
