@@ -304,29 +304,38 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t base_hi = smem_u32(a_slot(s, 0));
           const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
           mbar_wait_warp(&a_empty[s], ph ^ 1);
-          for (int u = warp; u < units && !(a.dbg & 1); u += PRODUCER_WARPS) {
-            const int32_t row = u * rows_per_unit + lane_row;
-            const int32_t Q = m0 + row;
-            const float* src = I;
-            int32_t w0 = -(1 << 20);
-            if (row < Rt && Q < a.Mp32) {
-              const int32_t bb = Q / hw_q;
-              const int32_t rem = Q - bb * hw_q;
-              const int32_t wo = rem / a.Hq, hq = rem - wo * a.Hq;
-              const int32_t h = a.s * hq + lane_pha - a.p;
-              if ((unsigned)h < (unsigned)a.h_i) {
-                w0 = a.s * wo - a.p;
-                src = I + (int64_t)bb * a.wim_ci * a.plane + (int64_t)w0 * a.h_i + h;
+          // UPI units in flight per iteration, as in the regular producer loop
+          for (int u = warp; u < units && !(a.dbg & 1); u += UPI * PRODUCER_WARPS) {
+            float v[UPI][BK];
+            int32_t row[UPI];
+#pragma unroll
+            for (int q = 0; q < UPI; ++q) {
+              row[q] = (u + q * PRODUCER_WARPS) * rows_per_unit + lane_row;
+              const int32_t Q = m0 + row[q];
+              const float* src = I;
+              int32_t w0 = -(1 << 20);
+              if (u + q * PRODUCER_WARPS < units && row[q] < Rt && Q < a.Mp32) {
+                const int32_t bb = Q / hw_q;
+                const int32_t rem = Q - bb * hw_q;
+                const int32_t wo = rem / a.Hq, hq = rem - wo * a.Hq;
+                const int32_t h = a.s * hq + lane_pha - a.p;
+                if ((unsigned)h < (unsigned)a.h_i) {
+                  w0 = a.s * wo - a.p;
+                  src = I + (int64_t)bb * a.wim_ci * a.plane + (int64_t)w0 * a.h_i + h;
+                }
+              }
+#pragma unroll
+              for (int e = 0; e < BK; ++e) {
+                // elements past ksteps*8 are never read by the MMAs: no loads for them
+                const int32_t w = w0 + a.wim_dw[e];
+                v[q][e] = (e < a.ksteps * 8 && (unsigned)w < (unsigned)a.w_i) ? ldg_stream(src + a.wim_off[e]) : 0.0f;
               }
             }
-            float v[BK];
 #pragma unroll
-            for (int e = 0; e < BK; ++e) {
-              // elements past ksteps*8 are never read by the MMAs: no loads for them
-              const int32_t w = w0 + a.wim_dw[e];
-              v[e] = (e < a.ksteps * 8 && (unsigned)w < (unsigned)a.w_i) ? ldg_stream(src + a.wim_off[e]) : 0.0f;
-            }
-            store_rows(row, v, base_hi + (uint32_t)lane_pha * slot_stride, base_lo + (uint32_t)lane_pha * slot_stride);
+            for (int q = 0; q < UPI; ++q)
+              if (u + q * PRODUCER_WARPS < units)
+                store_rows(row[q], v[q], base_hi + (uint32_t)lane_pha * slot_stride,
+                           base_lo + (uint32_t)lane_pha * slot_stride);
           }
           fence_proxy_async_smem();
           __syncwarp();
@@ -961,6 +970,7 @@ static const Cand kCands[] = {
     // or stride 2 with BN <= 128: 56x56 64->64 3% and 56->28 128 8% faster; slower where
     // the MMA or the filter stream binds)
     {4, 64, 0, 2, 8, 1, 2}, {2, 64, 0, 2, 8, 1, 2}, {1, 128, 0, 2, 4, 1, 2}, {2, 128, 0, 2, 6, 1, 2},
+    {2, 256, 0, 2, 4, 1, 2},  // 1x1 layers (14x14 1024->256 143 -> 121 us, 7x7 512->2048 124 -> 113 us)
     // 3xTF32 with a double-buffered (hi + lo) window: fits the stride-1 windows
     {2, 64, 1, 2, 4, 1, 1}, {1, 64, 1, 2, 6, 1, 1}, {2, 128, 1, 2, 3, 1, 1}, {1, 128, 1, 2, 4, 1, 1},
     {1, 256, 1, 2, 2, 1, 1},
@@ -968,8 +978,8 @@ static const Cand kCands[] = {
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
 constexpr int kFirstUpi2Cand = 38;
-constexpr int kFirstSplit2Cand = 42;  // 3xTF32 with two window slots
-constexpr int kFirstProbeCand = 47;  // candidates from here on are CGB_SW_CFG probes only
+constexpr int kFirstSplit2Cand = 43;  // 3xTF32 with two window slots
+constexpr int kFirstProbeCand = 48;  // candidates from here on are CGB_SW_CFG probes only
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st) {
@@ -1018,11 +1028,12 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(39, 2, 64, false, 2, 8, true, 2)
     CGB_SW_CASE(40, 1, 128, false, 2, 4, true, 2)
     CGB_SW_CASE(41, 2, 128, false, 2, 6, true, 2)
-    CGB_SW_CASE(42, 2, 64, true, 2, 4, true, 1)
-    CGB_SW_CASE(43, 1, 64, true, 2, 6, true, 1)
-    CGB_SW_CASE(44, 2, 128, true, 2, 3, true, 1)
-    CGB_SW_CASE(45, 1, 128, true, 2, 4, true, 1)
-    CGB_SW_CASE(46, 1, 256, true, 2, 2, true, 1)
+    CGB_SW_CASE(42, 2, 256, false, 2, 4, true, 2)
+    CGB_SW_CASE(43, 2, 64, true, 2, 4, true, 1)
+    CGB_SW_CASE(44, 1, 64, true, 2, 6, true, 1)
+    CGB_SW_CASE(45, 2, 128, true, 2, 3, true, 1)
+    CGB_SW_CASE(46, 1, 128, true, 2, 4, true, 1)
+    CGB_SW_CASE(47, 1, 256, true, 2, 2, true, 1)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -1075,7 +1086,10 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     const bool deep_first = bn == 256 && (n_tiles >= 2 || a.s == 1);
     // staging-bound layers (stride-2 windows with BN <= 128, or BN = 64) first try the
     // candidates with two units in flight per producer warp
-    const bool upi2 = (a.s == 2 && bn <= 128) || bn == 64;
+    // (and the 1x1 layers: one tap per staged row, the most staging-bound of all). In the
+    // w-im2col mode only the short rows (<= 16 elements: VGG conv1 289 vs 370 us) gain;
+    // the stem's 24-element rows run faster with one unit (401 vs 429 us).
+    const bool upi2 = a.wim ? a.ksteps <= 2 : ((a.s == 2 && bn <= 128) || bn == 64 || a.taps == 1);
     // try order: 3xTF32 double-buffered windows (split), two-unit producers (upi2), deep
     // filter rings (deep_first), then the regular table; probes never
     int order[kFirstProbeCand];
