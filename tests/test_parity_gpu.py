@@ -285,6 +285,9 @@ VARIANT_CASES = [
     # pad > k-1 and asymmetric periods: wrapped reads land in shared zero rows
     (dict(k_n=64, k_h=3, k_w=2, c_i=32, h_i=11, w_i=9, b=3, s=1, p=2), "tcgen05-shifted"),
     (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=20, w_i=20, b=2, s=3, p=1), "tcgen05-gather"),
+    # 1x1 with a wide filter tile (two-unit producers, BN = 256) and a deep one
+    (dict(k_n=256, k_h=1, k_w=1, c_i=96, h_i=20, w_i=20, b=40, s=1, p=0), "tcgen05-shifted"),
+    (dict(k_n=512, k_h=1, k_w=1, c_i=128, h_i=7, w_i=7, b=64, s=1, p=0), "tcgen05-shifted"),
     # low-channel layers: w-im2col rows (k_w*c_i <= 32 values per row), k_h taps as shifts
     (dict(k_n=64, k_h=7, k_w=7, c_i=3, h_i=40, w_i=40, b=2, s=2, p=3), "tcgen05-shifted-wim"),
     (dict(k_n=64, k_h=3, k_w=3, c_i=3, h_i=30, w_i=30, b=2, s=1, p=1), "tcgen05-shifted-wim"),
