@@ -134,7 +134,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         if (lane == 0) mbar_arrive(&empty[slot]);
       }
     }
-  } else if (warp < NW) {
+  } else if (warp < NW) {  // modes 0, 2, 3
     int k = 0;
     const int ipw = a.nph * a.ncol * a.nb_ldg;
     for (int w = blockIdx.x; w < a.windows; w += gridDim.x)
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
       // kernel lane mapping: stride 2 -> lanes cover 16 rows x both h phases = 32 consecutive h
       const int row = a.s == 2 ? (lane & 7) + 8 * (lane >> 4) + 16 * bx : lane + 32 * bx;
       const int pa = a.s == 2 ? (lane >> 3) & 1 : 0;
-      const int h = a.s * row + pa - a.p, wi = a.s * wq + pc - a.p;
+      const int h = a.s * row + pa - (mode == 3 ? 0 : a.p), wi = a.s * wq + pc - a.p;  // mode 3: 128B-aligned runs
       const bool ok = row < a.Hq && (unsigned)h < (unsigned)a.h_i && (unsigned)wi < (unsigned)a.w_i;
       const float* src = I + ((long)bb * a.c_i + 32L * cc) * plane + (long)wi * a.h_i + h;
       float v[32];
@@ -234,6 +234,7 @@ int main(int argc, char** argv) {
   printf("geometry %s: input %.1f MB, %.1f MB of window\n", s1 ? "56x56 c64 s1" : "56->28 c128 s2", n * 4 / 1e6,
          a.items * a.nph * a.Hq * 128 / 1e6);
   if (!only_tma) {
+    run<12, 12>("LDG aligned (mode 3)", I, a, 3, 5);
     run<12, 12>("LDG (mode 0)", I, a, 0, 5);
     run<16, 16>("LDG (mode 0)", I, a, 0, 5);
   }
