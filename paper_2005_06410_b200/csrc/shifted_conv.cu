@@ -122,6 +122,22 @@ CGB_DEV int sk_group_of(const Args& a, int x) {
   return c;
 }
 
+// One w-im2col row for a compile-time (k_w, c_i): element j = c + CI*kw, the w bound
+// checked once per kw and the offsets folded into immediates; zero past KW*CI.
+template <int KW, int CI>
+CGB_DEV void wim_row(const Args& a, const float* src, int32_t w0, float (&v)[32]) {
+  const int32_t plane = (int32_t)a.plane;
+#pragma unroll
+  for (int kw = 0; kw < KW; ++kw) {
+    const bool ok = (unsigned)(w0 + kw) < (unsigned)a.w_i;
+    const float* p = src + kw * a.h_i;
+#pragma unroll
+    for (int c = 0; c < CI; ++c) v[c + CI * kw] = ok ? ldg_stream(p + c * plane) : 0.0f;
+  }
+#pragma unroll
+  for (int j = KW * CI; j < 32; ++j) v[j] = 0.0f;
+}
+
 // First padded row of this CTA's part of a tile and its subtile count (MT, or tail_mt for
 // the tail m-tiles); pair tiles stack rank 0's and rank 1's rows.
 template <int MT, bool PAIR>
@@ -324,11 +340,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                   src = I + (int64_t)bb * a.wim_ci * a.plane + (int64_t)w0 * a.h_i + h;
                 }
               }
+              if (BN == 64 && a.wim_kw == 7 && a.wim_ci == 3) {
+                wim_row<7, 3>(a, src, w0, v[q]);  // the 7x7 stem: bound checks once per kw
+              } else if (BN == 64 && a.wim_kw == 3 && a.wim_ci == 3) {
+                wim_row<3, 3>(a, src, w0, v[q]);  // VGG conv1
+              } else {
 #pragma unroll
-              for (int e = 0; e < BK; ++e) {
-                // elements past ksteps*8 are never read by the MMAs: no loads for them
-                const int32_t w = w0 + a.wim_dw[e];
-                v[q][e] = (e < a.ksteps * 8 && (unsigned)w < (unsigned)a.w_i) ? ldg_stream(src + a.wim_off[e]) : 0.0f;
+                for (int e = 0; e < BK; ++e) {
+                  // elements past ksteps*8 are never read by the MMAs: no loads for them
+                  const int32_t w = w0 + a.wim_dw[e];
+                  v[q][e] = (e < a.ksteps * 8 && (unsigned)w < (unsigned)a.w_i) ? ldg_stream(src + a.wim_off[e]) : 0.0f;
+                }
               }
             }
 #pragma unroll
