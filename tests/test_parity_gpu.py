@@ -294,6 +294,12 @@ VARIANT_CASES = [
     (dict(k_n=32, k_h=3, k_w=3, c_i=1, h_i=17, w_i=13, b=3, s=1, p=0), "tcgen05-shifted-wim"),
     (dict(k_n=48, k_h=4, k_w=4, c_i=8, h_i=12, w_i=12, b=2, s=2, p=1), "tcgen05-shifted-wim"),
     (dict(k_n=96, k_h=5, k_w=3, c_i=5, h_i=20, w_i=16, b=2, s=1, p=2), "tcgen05-shifted-wim"),
+    # the specialised (k_w, c_i) = (7, 3) / (3, 3) producers at odd sizes, k_n = 64 (BN = 64)
+    (dict(k_n=64, k_h=7, k_w=7, c_i=3, h_i=37, w_i=29, b=3, s=2, p=3), "tcgen05-shifted-wim"),
+    (dict(k_n=64, k_h=3, k_w=3, c_i=3, h_i=23, w_i=41, b=2, s=1, p=1), "tcgen05-shifted-wim"),
+    (dict(k_n=64, k_h=3, k_w=3, c_i=3, h_i=23, w_i=41, b=2, s=2, p=0), "tcgen05-shifted-wim"),
+    # wide stride-2 image (halo beyond 256 rows per phase)
+    (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=301, w_i=40, b=1, s=2, p=1), "tcgen05-shifted"),
 ]
 
 
