@@ -320,12 +320,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t base_hi = smem_u32(a_slot(s, 0));
           const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
           mbar_wait_warp(&a_empty[s], ph ^ 1);
-          // UPI units in flight per iteration, as in the regular producer loop
-          for (int u = warp; u < units && !(a.dbg & 1); u += UPI * PRODUCER_WARPS) {
-            float v[UPI][BK];
-            int32_t row[UPI];
+          // One unit in flight per iteration: a second one (the regular loop's UPI = 2)
+          // raised the register pressure of the two-unit kernels for every layer.
+          constexpr int WU = 1;
+          for (int u = warp; u < units && !(a.dbg & 1); u += WU * PRODUCER_WARPS) {
+            float v[WU][BK];
+            int32_t row[WU];
 #pragma unroll
-            for (int q = 0; q < UPI; ++q) {
+            for (int q = 0; q < WU; ++q) {
               row[q] = (u + q * PRODUCER_WARPS) * rows_per_unit + lane_row;
               const int32_t Q = m0 + row[q];
               const float* src = I;
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               }
             }
 #pragma unroll
-            for (int q = 0; q < UPI; ++q)
+            for (int q = 0; q < WU; ++q)
               if (u + q * PRODUCER_WARPS < units)
                 store_rows(row[q], v[q], base_hi + (uint32_t)lane_pha * slot_stride,
                            base_lo + (uint32_t)lane_pha * slot_stride);
