@@ -1108,12 +1108,13 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     // tiles, or with a stride-1 (small) window that leaves the shared memory for them
     // (14x14 256->256: 62 -> 57 us); stride-2 windows keep the L1 instead
     const bool deep_first = bn == 256 && (n_tiles >= 2 || a.s == 1);
-    // staging-bound layers (stride-2 windows with BN <= 128, or BN = 64) first try the
-    // candidates with two units in flight per producer warp
-    // (and the 1x1 layers: one tap per staged row, the most staging-bound of all). In the
-    // w-im2col mode only the short rows (<= 16 elements: VGG conv1 289 vs 370 us) gain;
-    // the stem's 24-element rows run faster with one unit (401 vs 429 us).
-    const bool upi2 = a.wim ? a.ksteps <= 2 : ((a.s == 2 && bn <= 128) || bn == 64 || a.taps == 1);
+    // staging-bound layers (stride-2 windows with BN <= 128) first try the candidates with
+    // two units in flight per producer warp (and the 1x1 layers: one tap per staged row,
+    // the most staging-bound of all): s2 56->28 128 87 vs 97 us. Stride-1 BN = 64 layers
+    // no longer gain (56x56 64->64: 74.8 vs 73.3 us with one unit, same box, alternated).
+    // The w-im2col producer stages one unit per iteration in either kernel; VGG conv1
+    // runs equally fast in both (266-270 us), so its old rule (short rows) stays.
+    const bool upi2 = a.wim ? a.ksteps <= 2 : ((a.s == 2 && bn <= 128) || a.taps == 1);
     // try order: 3xTF32 double-buffered windows (split), two-unit producers (upi2), deep
     // filter rings (deep_first), then the regular table; probes never
     int order[kFirstProbeCand];
