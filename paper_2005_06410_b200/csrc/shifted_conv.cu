@@ -442,7 +442,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int n0 = (tile / a.m_tiles) * BN + (int)rank * C::NB;
         for (int cc = cc0; cc < cc1; ++cc)
           for (int tap = 0; tap < a.taps; ++tap) {
-            mbar_wait_spin(&b_empty[bs], bph ^ 1);  // WAR on own smem: CTA scope suffices
+            // WAR on own smem: CTA scope suffices. A suspending try_wait, not a spin: the
+            // ring is deep enough to hide the wake-up, and the spinning thread took issue
+            // slots from the producer warps of its sub-partition (BN = 256 layers 0.5-1%).
+            mbar_wait(&b_empty[bs], bph ^ 1);
             if (a.dbg & 8) {
               if (PAIR) mbar_arrive_cluster(lead_b_full + bs * 8);
               else mbar_arrive(&b_full[bs]);
