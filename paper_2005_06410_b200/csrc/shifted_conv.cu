@@ -81,10 +81,25 @@ struct Args {
   int32_t wim_kw, wim_ci;  // the real k_w and c_i in that mode (k_w = 1 and c_i = 32 above)
   int32_t wim_off[32];     // w-im2col element j = c + c_i*kw: c*plane + kw*h_i (constant bank, uniform)
   int32_t wim_dw[32];      //   and its kw (a large negative value past k_w*c_i)
+  // n / (Hq*Wq) and n / Hq as a multiply-shift (n < 2^31): the producers' per-row
+  // padded-plane decomposition without integer-division sequences
+  uint32_t fd_hwq_m, fd_hwq_p, fd_hq_m, fd_hq_p;
   unsigned long long* stats;  // per-CTA cycle counters when dbg & 64 (profiling only)
   int32_t dbg;        // profiling switches (CGB_DEBUG_SW): 1 = producers skip loads, 2 = skip MMAs,
                       //   4 = skip epilogue stores, 8 = skip filter TMA
 };
+
+// floor(n / d) for 0 <= n < 2^31 with m = ceil(2^p / d), p = 31 + ceil(log2 d): the
+// error n*(m - 2^p/d)/2^p < 1/d never crosses an integer (m fits 32 bits for every d).
+CGB_DEV int32_t fast_div(int32_t n, uint32_t m, uint32_t p) {
+  return (int32_t)(((uint64_t)(uint32_t)n * m) >> p);
+}
+inline void fast_div_magic(uint32_t d, uint32_t& m, uint32_t& p) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  p = 31 + l;
+  m = (uint32_t)(((1ull << p) + d - 1) / d);
+}
 
 // Segment sequence of one group: first the pieces of its stream-K unit range
 // [sk_begin(gid), sk_begin(gid+1)) over tiles [0, sk_tiles), cut at tile boundaries;
@@ -273,9 +288,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int32_t Q = m0 + row;
       ok = row < Rt && Q < a.Mp32;
       if (!ok) return I;
-      const int32_t bb = Q / hw_q;
+      const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
       const int32_t rem = Q - bb * hw_q;
-      const int32_t wq = rem / a.Hq, hq = rem - wq * a.Hq;
+      const int32_t wq = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wq * a.Hq;
       const int32_t h = a.s * hq + ph_a - a.p, w = a.s * wq + ph_c - a.p;
       ok = (unsigned)h < (unsigned)a.h_i && (unsigned)w < (unsigned)a.w_i;
       return I + ((int64_t)bb * a.c_i + (int64_t)cc * BK) * a.plane + (w * a.h_i + h);
@@ -333,9 +348,9 @@ __global__ void __launch_bounds__(THREADS, 1)
               const float* src = I;
               int32_t w0 = -(1 << 20);
               if (u + q * PRODUCER_WARPS < units && row[q] < Rt && Q < a.Mp32) {
-                const int32_t bb = Q / hw_q;
+                const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
                 const int32_t rem = Q - bb * hw_q;
-                const int32_t wo = rem / a.Hq, hq = rem - wo * a.Hq;
+                const int32_t wo = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wo * a.Hq;
                 const int32_t h = a.s * hq + lane_pha - a.p;
                 if ((unsigned)h < (unsigned)a.h_i) {
                   w0 = a.s * wo - a.p;
@@ -392,7 +407,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int q = 0; q < UPI; ++q) {
             const int uq = u + q * PRODUCER_WARPS;
-            const int pc = uq / row_blocks, rb = uq - pc * row_blocks;
+            const int pc = a.nph_w == 1 ? 0 : uq / row_blocks, rb = uq - pc * row_blocks;
             row[q] = rb * rows_per_unit + lane_row;
             off[q] = (uint32_t)(lane_pha + a.nph_h * pc) * slot_stride;
             src[q] = row_src(row[q], lane_pha, pc, m0, cc, ok[q]);
@@ -633,9 +648,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
         int64_t P = -1;
         if (Q < a.Mp32) {
-          const int32_t bb = Q / hw_q;
+          const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
           const int32_t rem = Q - bb * hw_q;
-          const int32_t wq = rem / a.Hq, hq = rem - wq * a.Hq;
+          const int32_t wq = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wq * a.Hq;
           if (hq < a.h_o && wq < a.w_o) P = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
         }
         const uint32_t trow = tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS + mt * BN;
@@ -785,6 +800,8 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
   a.R = MT * 128 + a.dmax;
   a.R_pad = (a.R + 7) / 8 * 8;
+  fast_div_magic((uint32_t)(a.Hq * a.Wq), a.fd_hwq_m, a.fd_hwq_p);
+  fast_div_magic((uint32_t)a.Hq, a.fd_hq_m, a.fd_hq_p);
   const uint32_t a_slot_bytes = (uint32_t)(a.NPH * a.R_pad * 128);
   const size_t base_smem = (size_t)A_SLOTS * C::NS * a_slot_bytes + (size_t)B_STAGES * C::NS * C::B_TILE + 1024 + 1024;
   if (base_smem > 227 * 1024) return cudaErrorNotSupported;
