@@ -407,7 +407,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int q = 0; q < UPI; ++q) {
             const int uq = u + q * PRODUCER_WARPS;
-            const int pc = a.nph_w == 1 ? 0 : uq / row_blocks, rb = uq - pc * row_blocks;
+            // phase column: nph_w <= 2 (stride <= 2), so a compare instead of a division
+            const int pc = uq >= row_blocks ? 1 : 0, rb = uq - pc * row_blocks;
             row[q] = rb * rows_per_unit + lane_row;
             off[q] = (uint32_t)(lane_pha + a.nph_h * pc) * slot_stride;
             src[q] = row_src(row[q], lane_pha, pc, m0, cc, ok[q]);
