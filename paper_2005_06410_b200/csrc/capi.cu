@@ -129,6 +129,20 @@ cudaError_t make_filter_tmap_tapmajor(CUtensorMap* tm, const float* f, const Con
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+cudaError_t make_input_tmap_1x1(CUtensorMap* tm, const float* i, const ConvGeom& g) {
+  auto enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  const int64_t hw = g.h_i * g.w_i;
+  cuuint64_t dims[3] = {(cuuint64_t)hw, (cuuint64_t)g.c_i, (cuuint64_t)g.b};
+  cuuint64_t strides[2] = {(cuuint64_t)(hw * 4), (cuuint64_t)(hw * g.c_i * 4)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(i), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // ------------------------------------------------------------------ workspace (ScratchTracker)
 struct Scratch {
   std::mutex mu;

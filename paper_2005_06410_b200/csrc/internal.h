@@ -53,6 +53,8 @@ cudaError_t make_filter_tmap(CUtensorMap* tm, const float* f, int64_t k_n, int64
 // 3-D TMA descriptor over F seen as (k_n, tap = i_kh + i_kw*k_h, c_i): box 32 filters x
 // 1 tap x 32 channels, 32-byte-atom 128B swizzle. Needs k_n % 4 == 0.
 cudaError_t make_filter_tmap_tapmajor(CUtensorMap* tm, const float* f, const ConvGeom& g);
+// I viewed as (h*w pixels, c_i, b) with 32 x 32 x 1 boxes, SW128 32-byte atoms (1x1 layers)
+cudaError_t make_input_tmap_1x1(CUtensorMap* tm, const float* i, const ConvGeom& g);
 
 // K3 tap-major gather kernel (tc_gather.cu): c_i >= 16, k_n % 4 == 0.
 bool gather_supported(const ConvGeom& g);

@@ -77,6 +77,7 @@ struct Args {
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
   int32_t pstore;     // epilogue stores: 1 lane pairs 64 B (default), 0 per-lane 32 B (CGB_SW_PSTORE=0)
+  int32_t tma_a;      // 1x1 layers: A (pixels x channels) TMA'd MN-major straight from I, no staging
   int32_t wim;        // w-im2col mode: a row holds the k_w*c_i values of one output row's w-taps
   int32_t wim_kw, wim_ci;  // the real k_w and c_i in that mode (k_w = 1 and c_i = 32 above)
   int32_t wim_off[32];     // w-im2col element j = c + c_i*kw: c*plane + kw*h_i (constant bank, uniform)
@@ -224,7 +225,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == TMA_WARP) {
     if (lane == 0) {
       for (int s = 0; s < A_SLOTS; ++s) {
-        mbar_init(&a_full[s], PAIR ? 2 : PRODUCER_WARPS);  // pairs: one forwarded arrive per CTA
+        // pairs: one forwarded arrive per CTA; TMA-fed A: the loader's expect_tx arrive
+        mbar_init(&a_full[s], a.tma_a ? 1 : (PAIR ? 2 : PRODUCER_WARPS));
         mbar_init(&a_ready[s], PRODUCER_WARPS);
         mbar_init(&a_empty[s], 1);
       }
@@ -320,7 +322,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     };
     int tile, cc0, cc1;
-    if (a.wim) {
+    if (a.tma_a) {
+      // A arrives by TMA (filter warp): nothing to stage
+    } else if (a.wim) {
       // ---- w-im2col rows (low-channel layers): row (h-phase pha, hq, wo, image) holds
       // I(s*hq + pha - p, s*wo + kw - p, c) at element j = c + c_i*kw (zero past k_w*c_i and
       // in the padding); only the k_h taps are row shifts. One chunk per tile.
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- window forwarder
     // A cluster-scope release arrive costs a GPU-wide memory barrier; paying it once per
     // chunk here keeps it off the producer warps (the bottleneck of staging-bound layers).
-    if (PAIR && lane == 0) {
+    if (PAIR && lane == 0 && !a.tma_a) {
       int it = 0, tile, cc0, cc1;
       for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j)
         for (int cc = cc0; cc < cc1; ++cc, ++it) {
@@ -454,9 +458,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t bph = 0;
       const uint32_t b0_hi = smem_u32(b_slot(0, 0)), b0_lo = smem_u32(b_slot(0, SPLIT ? 1 : 0));
       int tile, cc0, cc1;
+      int ait = 0;  // TMA-fed A: chunk counter (window slot ring)
       for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
         const int n0 = (tile / a.m_tiles) * BN + (int)rank * C::NB;
-        for (int cc = cc0; cc < cc1; ++cc)
+        int32_t am0 = 0;
+        int amtc = 0;
+        if (a.tma_a) tile_rows<MT, PAIR>(a, tile, rank, am0, amtc);
+        for (int cc = cc0; cc < cc1; ++cc) {
+          if (a.tma_a) {
+            // 1x1 layers: the A tile is MT x 4 boxes of 32 pixels x 32 channels, MN-major
+            // SW128 (32-byte atoms) like the filter tiles; rows past an image's hw (padded
+            // to 32) and past the batch are zero-filled by the TMA unit.
+            const int s = ait % A_SLOTS;
+            mbar_wait(&a_empty[s], ((ait / A_SLOTS) & 1) ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&a_full[s], (uint32_t)amtc * 16384u * (PAIR ? 2u : 1u));
+            const uint32_t dst0 = smem_u32(a_slot(s, 0));
+            for (int q = 0; q < amtc * 4; ++q) {
+              const int32_t Q = am0 + q * 32;
+              const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
+              const int32_t px = Q - bb * a.Hq;
+              if (PAIR) tma_load_3d_2sm(dst0 + q * 4096, &tmap_lo, lead_a_full + s * 8, px, cc * BK, bb);
+              else tma_load_3d(dst0 + q * 4096, &tmap_lo, &a_full[s], px, cc * BK, bb);
+            }
+            ++ait;
+          }
           for (int tap = 0; tap < a.taps; ++tap) {
             // WAR on own smem: CTA scope suffices. A suspending try_wait, not a spin: the
             // ring is deep enough to hide the wake-up, and the spinning thread took issue
@@ -484,6 +509,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             if (++bs == B_STAGES) { bs = 0; bph ^= 1; }
           }
+        }
       }
     }
   } else if (warp == MMA_WARP) {
@@ -497,7 +523,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       tap_shift[t] = (uint32_t)((phase * a.R_pad + kh / a.s + a.Hq * (kw / a.s)) * 8);
     }
     __syncwarp();
-    constexpr uint32_t idesc = idesc_tf32(C::UMMA_N, false, true, PAIR ? 256 : 128);
+    constexpr uint32_t idesc_k = idesc_tf32(C::UMMA_N, false, true, PAIR ? 256 : 128);
+    constexpr uint32_t idesc_mn = idesc_tf32(C::UMMA_N, true, true, PAIR ? 256 : 128);
+    const uint32_t idesc = a.tma_a ? idesc_mn : idesc_k;  // TMA-fed A is MN-major
     if (rank == 0 && elect_one()) {
       // Descriptors are built once per operand slot; per UMMA only the 14-bit start
       // address field moves (row shift d*128 B = d*8 units, k-step 32 B = 2 units,
@@ -508,7 +536,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       unsigned long long w_t = 0, w_a = 0, w_b = 0, t_start = clock64();
       if (a.dbg & 64) a.stats[blockIdx.x * 16 + 9] = gtimer();
       const bool st = (a.dbg & 64) != 0;
-      const uint64_t a_desc0 = smem_desc(smem_u32(a_slot(0, 0)), 16, 1024);
+      // K-major window (128-byte rows, k-step 32 B = 2 units) or, TMA-fed, MN-major 32-pixel
+      // blocks like the filter tiles (k-step = 8 channel rows of 128 B = 64 units)
+      const uint64_t a_desc0 = a.tma_a ? smem_desc(smem_u32(a_slot(0, 0)), 4096, 512, 0, kLayoutSW128_32B)
+                                       : smem_desc(smem_u32(a_slot(0, 0)), 16, 1024);
+      const uint32_t a_kstep = a.tma_a ? 64u : 2u;
       const uint64_t a_lo_off = SPLIT ? (uint64_t)(a_slot_bytes >> 4) : 0;  // lo window follows hi
       const uint64_t a_slot_units = (uint64_t)(C::NS * a_slot_bytes) >> 4;
       const uint64_t b_desc0 = smem_desc(smem_u32(b_slot(0, 0)), 4096, 512, 0, kLayoutSW128_32B);
@@ -556,12 +588,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                   for (int mt = 0; mt < MT; ++mt) {
                     if (mt >= mtc) break;  // tail tile: fewer M subtiles
-                    const uint64_t ad = at + (uint64_t)(mt * 1024 + kk * 2);
+                    const uint64_t ad = at + (uint64_t)(mt * 1024 + kk * a_kstep);
                     const uint64_t bd = bt + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
                     const uint32_t d = d_base + mt * BN + hf * C::UMMA_N;
                     const uint32_t acc = kk == 0 ? first : 1u;
                     if (SPLIT) {
-                      const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024 + kk * 2);
+                      const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024 + kk * a_kstep);
                       const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
                       if (PAIR) {
                         mma_tf32_2cta(d, ad_lo, bd, idesc, acc);
@@ -953,6 +985,7 @@ static Args make_args(const ConvGeom& g) {
   const char* ps = getenv("CGB_SW_PSTORE");
   a.pstore = ps ? atoi(ps) : 1;
   a.wim = 0; a.wim_kw = 1; a.wim_ci = a.c_i;
+  a.tma_a = 0;
   const char* dbg = getenv("CGB_DEBUG_SW");
   a.dbg = dbg ? atoi(dbg) : 0;
   a.stats = nullptr;
@@ -1135,7 +1168,7 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     // no longer gain (56x56 64->64: 74.8 vs 73.3 us with one unit, same box, alternated).
     // The w-im2col producer stages one unit per iteration in either kernel; VGG conv1
     // runs equally fast in both (266-270 us), so its old rule (short rows) stays.
-    const bool upi2 = a.wim ? a.ksteps <= 2 : ((a.s == 2 && bn <= 128) || a.taps == 1);
+    const bool upi2 = a.wim ? a.ksteps <= 2 : ((a.s == 2 && bn <= 128) || (a.taps == 1 && !a.tma_a));
     // try order: 3xTF32 double-buffered windows (split), two-unit producers (upi2), deep
     // filter rings (deep_first), then the regular table; probes never
     int order[kFirstProbeCand];
@@ -1177,6 +1210,26 @@ cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t
     if ((e = make_filter_tmap_tapmajor(&tl, f_lo, g)) != cudaSuccess) return e;
   } else {
     tl = th;
+  }
+  // 1x1 stride-1 layers in TF32: A straight from I by TMA (pixels are contiguous per
+  // channel plane, i.e. MN-major), no producer staging. Needs 16-byte channel-plane
+  // strides (h*w % 4 == 0) and a 16-byte aligned I; rows are the pixels of each image
+  // padded to a multiple of 32 (the TMA box), so the plane is (hw32 x 1) per image.
+  const char* te = getenv("CGB_SW_TMA_A");
+  const int64_t hw = g.h_i * g.w_i;
+  if (!split && g.k_h == 1 && g.k_w == 1 && g.s == 1 && g.p == 0 && hw % 4 == 0 &&
+      reinterpret_cast<uintptr_t>(I) % 16 == 0 && !(te && atoi(te) == 0)) {
+    const int64_t hwp = (hw + 31) / 32 * 32;
+    if ((hwp * g.b) < (int64_t(1) << 30) && make_input_tmap_1x1(&tl, I, g) == cudaSuccess) {
+      a.tma_a = 1;
+      a.Hq = (int32_t)hwp;
+      a.Wq = 1;
+      a.h_o = (int32_t)hw;
+      a.w_o = 1;
+      a.dmax = 0;
+      a.Mp = hwp * g.b;
+      a.Mp32 = (int32_t)a.Mp;
+    }
   }
   static int sms = 0;
   if (!sms) {

@@ -285,6 +285,11 @@ VARIANT_CASES = [
     # pad > k-1 and asymmetric periods: wrapped reads land in shared zero rows
     (dict(k_n=64, k_h=3, k_w=2, c_i=32, h_i=11, w_i=9, b=3, s=1, p=2), "tcgen05-shifted"),
     (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=20, w_i=20, b=2, s=3, p=1), "tcgen05-gather"),
+    # 1x1 stride 1 with h*w % 4 == 0: A TMA'd straight from I (MN-major, TF32), pixel
+    # planes not a multiple of the 32-pixel box, partial channel chunks, odd batches
+    (dict(k_n=96, k_h=1, k_w=1, c_i=40, h_i=10, w_i=10, b=5, s=1, p=0), "tcgen05-shifted"),
+    (dict(k_n=64, k_h=1, k_w=1, c_i=32, h_i=12, w_i=12, b=7, s=1, p=0), "tcgen05-shifted"),
+    (dict(k_n=256, k_h=1, k_w=1, c_i=200, h_i=8, w_i=6, b=33, s=1, p=0), "tcgen05-shifted"),
     # 1x1 with a wide filter tile (two-unit producers, BN = 256) and a deep one
     (dict(k_n=256, k_h=1, k_w=1, c_i=96, h_i=20, w_i=20, b=40, s=1, p=0), "tcgen05-shifted"),
     (dict(k_n=512, k_h=1, k_w=1, c_i=128, h_i=7, w_i=7, b=64, s=1, p=0), "tcgen05-shifted"),
@@ -301,6 +306,24 @@ VARIANT_CASES = [
     # wide stride-2 image (halo beyond 256 rows per phase)
     (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=301, w_i=40, b=1, s=2, p=1), "tcgen05-shifted"),
 ]
+
+
+@pytest.mark.parametrize("cp", [
+    dict(k_n=256, k_h=1, k_w=1, c_i=64, h_i=56, w_i=56, b=3, s=1, p=0),
+    dict(k_n=96, k_h=1, k_w=1, c_i=40, h_i=10, w_i=10, b=5, s=1, p=0),
+    dict(k_n=512, k_h=1, k_w=1, c_i=1024, h_i=14, w_i=14, b=2, s=1, p=0),
+])
+def test_tma_fed_1x1_bitwise_equal_to_staged(monkeypatch, cp):
+    # TF32 1x1: the TMA-fed A tile (MN-major, straight from I) and the producer-staged
+    # K-major window feed the same fp32 bits to the same UMMAs in the same order
+    F, I = rand_inputs(cp, 4242)
+    Fd, Id = to_dev(F), to_dev(I)
+    monkeypatch.setenv("CGB_SW_TMA_A", "0")
+    staged = to_host(cg.conv(Fd, Id, cp, algo="fused", precision="tf32"))
+    monkeypatch.setenv("CGB_SW_TMA_A", "1")
+    tma = to_host(cg.conv(Fd, Id, cp, algo="fused", precision="tf32"))
+    assert cg.last_path() == "tcgen05-shifted"
+    assert np.array_equal(staged.view(np.uint32), tma.view(np.uint32))
 
 
 @pytest.mark.parametrize("case", range(len(VARIANT_CASES)))
