@@ -1052,12 +1052,16 @@ static const Cand kCands[] = {
     // 3xTF32 with a double-buffered (hi + lo) window: fits the stride-1 windows
     {2, 64, 1, 2, 4, 1, 1}, {1, 64, 1, 2, 6, 1, 1}, {2, 128, 1, 2, 3, 1, 1}, {1, 128, 1, 2, 4, 1, 1},
     {1, 256, 1, 2, 2, 1, 1},
+    // TMA-fed A (1x1 layers): no window to stage, so the A ring can be four chunks deep to
+    // cover the DRAM latency of the A tiles
+    {2, 256, 0, 4, 4, 1, 1}, {2, 128, 0, 4, 6, 1, 1},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
 constexpr int kFirstUpi2Cand = 38;
 constexpr int kFirstSplit2Cand = 43;  // 3xTF32 with two window slots
-constexpr int kFirstProbeCand = 48;  // candidates from here on are CGB_SW_CFG probes only
+constexpr int kFirstTmaACand = 48;   // deep A rings, tried first when a.tma_a
+constexpr int kFirstProbeCand = 50;  // candidates from here on are CGB_SW_CFG probes only
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st) {
@@ -1112,6 +1116,8 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(45, 2, 128, true, 2, 3, true, 1)
     CGB_SW_CASE(46, 1, 128, true, 2, 4, true, 1)
     CGB_SW_CASE(47, 1, 256, true, 2, 2, true, 1)
+    CGB_SW_CASE(48, 2, 256, false, 4, 4, true, 1)
+    CGB_SW_CASE(49, 2, 128, false, 4, 6, true, 1)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -1174,7 +1180,10 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     int order[kFirstProbeCand];
     int no = 0;
     if (split)
-      for (int i = kFirstSplit2Cand; i < kFirstProbeCand; ++i) order[no++] = i;
+      for (int i = kFirstSplit2Cand; i < kFirstTmaACand; ++i) order[no++] = i;
+    const char* tdeep = getenv("CGB_SW_TMA_DEEP");  // A/B switch for the deep A rings
+    if (a.tma_a && !(tdeep && atoi(tdeep) == 0))
+      for (int i = kFirstTmaACand; i < kFirstProbeCand; ++i) order[no++] = i;
     if (upi2)
       for (int i = kFirstUpi2Cand; i < kFirstSplit2Cand; ++i) order[no++] = i;
     if (deep_first)
@@ -1184,7 +1193,7 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
       const int i = order[k];
       const Cand& c = kCands[i];
       if (c.bn != bn || c.split != (int)split || c.mt > mt_max || c.pair != want_pair) continue;
-      if (pass % 2 == 0 && c.as != 2) continue;
+      if (pass % 2 == 0 && c.as < 2) continue;
       cudaError_t e = launch_cand(i, th, tl, I, O, a, st);
       if (e != cudaErrorNotSupported) {
         if (getenv("CGB_SW_VERBOSE"))
