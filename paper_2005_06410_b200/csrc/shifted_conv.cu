@@ -1052,7 +1052,7 @@ static const Cand kCands[] = {
     // 3xTF32 with a double-buffered (hi + lo) window: fits the stride-1 windows
     {2, 64, 1, 2, 4, 1, 1}, {1, 64, 1, 2, 6, 1, 1}, {2, 128, 1, 2, 3, 1, 1}, {1, 128, 1, 2, 4, 1, 1},
     {1, 256, 1, 2, 2, 1, 1},
-    // TMA-fed A (1x1 layers): no window to stage, so the A ring can be four chunks deep to
+    // 1x1 layers (TMA-fed A, or staged windows without halo): A rings four chunks deep
     // cover the DRAM latency of the A tiles
     {2, 256, 0, 4, 4, 1, 1}, {2, 128, 0, 4, 6, 1, 1},
 };
@@ -1060,7 +1060,7 @@ constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
 constexpr int kFirstUpi2Cand = 38;
 constexpr int kFirstSplit2Cand = 43;  // 3xTF32 with two window slots
-constexpr int kFirstTmaACand = 48;   // deep A rings, tried first when a.tma_a
+constexpr int kFirstTmaACand = 48;   // deep A rings, tried first for 1x1 layers
 constexpr int kFirstProbeCand = 50;  // candidates from here on are CGB_SW_CFG probes only
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
@@ -1182,7 +1182,9 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     if (split)
       for (int i = kFirstSplit2Cand; i < kFirstTmaACand; ++i) order[no++] = i;
     const char* tdeep = getenv("CGB_SW_TMA_DEEP");  // A/B switch for the deep A rings
-    if (a.tma_a && !(tdeep && atoi(tdeep) == 0))
+    // (staged 1x1 windows are as small -- no halo -- and gain too: 7x7 2048->512
+    // 121 -> 100 us, 512->2048 96 -> 87 us)
+    if ((a.tma_a || (a.taps == 1 && !a.wim)) && !split && !(tdeep && atoi(tdeep) == 0))
       for (int i = kFirstTmaACand; i < kFirstProbeCand; ++i) order[no++] = i;
     if (upi2)
       for (int i = kFirstUpi2Cand; i < kFirstSplit2Cand; ++i) order[no++] = i;
@@ -1192,7 +1194,11 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     for (int k = 0; k < no; ++k) {
       const int i = order[k];
       const Cand& c = kCands[i];
-      if (c.bn != bn || c.split != (int)split || c.mt > mt_max || c.pair != want_pair) continue;
+      // The deep-A-ring 1x1 candidates (MT = 2) beat the cost model's MT = 1 choice while
+      // their tiles fill at least half a round (7x7 2048->512: 100 vs 121 us).
+      const bool deep_a = i >= kFirstTmaACand && i < kFirstProbeCand &&
+                          (a.Mp + 511) / 512 * n_tiles >= (want_pair ? sms / 2 : sms) / 2;
+      if (c.bn != bn || c.split != (int)split || (c.mt > mt_max && !deep_a) || c.pair != want_pair) continue;
       if (pass % 2 == 0 && c.as < 2) continue;
       cudaError_t e = launch_cand(i, th, tl, I, O, a, st);
       if (e != cudaErrorNotSupported) {
