@@ -95,8 +95,10 @@ struct Args {
   int64_t n, ldb, plane;
 };
 
+// Min blocks per SM: unset for the implicit kernel (80 registers, unchanged SASS); 2 for
+// the explicit one, which needs 96 (at the default 64-register allocation it spilled).
 template <bool EXPLICIT>
-__global__ void __launch_bounds__(THREADS) ffma_conv_kernel(const float* __restrict__ F,
+__global__ void __launch_bounds__(THREADS, EXPLICIT ? 2 : 0) ffma_conv_kernel(const float* __restrict__ F,
                                                             const float* __restrict__ I,
                                                             const float* __restrict__ Bexp,
                                                             float* __restrict__ O, Args a) {
