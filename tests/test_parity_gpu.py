@@ -429,3 +429,28 @@ def test_unaligned_user_pointers(orc, prec):
         O = _offset_tensor4(np.zeros((64, h_o, w_o, 3), np.float32), 1)
         cg.conv(_offset_tensor4(F, 1), _offset_tensor4(I, 3), cp, algo=algo, precision=prec, out=O)
         assert per_output_error(to_host(O), ref, orc.output_scale(F, I, cp)) <= TOL[prec], (algo, cg.last_path())
+
+
+# ------------------------------------------- TF32 operand semantics (DESIGN §9 item 2)
+def _trunc_tf32(x):
+    return (np.asarray(x, np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+@pytest.mark.parametrize("kh,hi,s,p", [(1, 16, 1, 0), (1, 7, 1, 0), (3, 16, 1, 1), (3, 16, 2, 1)])
+def test_tf32_truncates_raw_operands(kh, hi, s, p):
+    """kind::tf32 drops the low 13 mantissa bits of the raw fp32 operands (truncation):
+    with one nonzero (tap, channel) per output, O = trunc(F)·trunc(I) exactly (two
+    11-bit mantissas multiply exactly in fp32). The 3xTF32 split relies on this."""
+    kn, ci, b = 128, 32, 2
+    rng = np.random.default_rng(7)
+    F = np.zeros((kn, kh, kh, ci), np.float32, order="F")
+    F[:, kh // 2, kh // 2, 3] = rng.uniform(0.5, 2.0, kn).astype(np.float32)
+    I = np.zeros((hi, hi, ci, b), np.float32, order="F")
+    I[:, :, 3, :] = rng.uniform(-2.0, 2.0, (hi, hi, b)).astype(np.float32)
+    cp = dict(k_n=kn, k_h=kh, k_w=kh, c_i=ci, h_i=hi, w_i=hi, b=b, s=s, p=p)
+    O = to_host(cg.conv(to_dev(F), to_dev(I), cp, precision="tf32"))
+    # centre tap with padding p = kh // 2: output (oh, ow) reads input (oh·s, ow·s)
+    Ic = _trunc_tf32(I[::s, ::s, 3, :])
+    want = _trunc_tf32(F[:, kh // 2, kh // 2, 3])[:, None, None, None] * Ic[None]
+    assert O.shape == want.shape
+    assert np.array_equal(O, want.astype(np.float32))
