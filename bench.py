@@ -30,6 +30,20 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+
+def _load_configs():
+    # by file path: importing the package would load libconvgemm_b200.so into the
+    # reference arm's process, which must run the reference alone
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("cgb_configs", os.path.join(ROOT, "paper_2005_06410_b200", "configs.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+CONFIGS = _load_configs()
+layer_seed = CONFIGS.layer_seed
+
 METRIC = "conv GFLOPS (2·k_n·h_o·w_o·b·k_h·k_w·c_i/s) per layer & % TF32 TC roofline"
 UNIT = "GFLOPS"
 BATCH = 128
@@ -285,7 +299,7 @@ def make_layer_tensors(cg, torch, layers, b, rank, world, seed=20177):
         cp = layer_cp(layer, b)
         h_o, w_o = out_hw(cp)
         F = cg.empty_tensor4(cp["k_n"], 3, 3, cp["c_i"])
-        gf = torch.Generator(device="cuda").manual_seed(seed + hash(layer[0]) % 1000)
+        gf = torch.Generator(device="cuda").manual_seed(layer_seed(layer[0], seed))  # stable (crc32) per layer
         F.copy_(torch.rand(F.shape, generator=gf, device="cuda") * 2 - 1)
         if world > 1:
             from paper_2005_06410_b200.shard import broadcast_filters
