@@ -125,6 +125,17 @@ void cgb_scratch_reset_peak(void);
 void cgb_scratch_set_limit(uint64_t bytes);
 void cgb_scratch_release(void); /* free the cached workspace */
 
+/* ---- dispatch policy (no reference equivalent: the reference's BlockingParams are
+ * CPU cache blocking, validated and otherwise ignored here) ----
+ * Keys: "sk" (stream-K: 0 never, 1 auto, 2 always), "tail" (tail tiles: 0/1/2), "pair"
+ * (CTA pairs allowed), "cfg" (force a kernel candidate, -1 auto), "mt", "bn" (force
+ * tile sizes, 0 auto), "tma_a", "tma_deep" (1x1-layer variants), "pstore", "pdl",
+ * "verbose", "smem_pad_kb", "host_chunk_kb", "host_no_bounce", "host_copy_threads",
+ * "debug" (profiling builds only). Every setting gives a correct result; unknown keys
+ * return CGB_INVALID_ARGUMENT. The library reads no environment variables. */
+cgb_status cgb_set_tuning(const char* key, int64_t value);
+cgb_status cgb_get_tuning(const char* key, int64_t* value);
+
 /* ---- diagnostics ---- */
 const char* cgb_last_error(void);
 const char* cgb_version(void);
@@ -133,9 +144,10 @@ uint64_t cgb_kernel_launch_count(void);
 /* Kernel path the last cgb_conv chose on this thread: 0 none, 1 tcgen05 implicit,
  * 2 tcgen05 explicit, 3 ffma implicit, 4 ffma explicit. */
 int cgb_last_path(void);
-/* Profiling hook: per-CTA MMA-issuer cycle counters of the last shifted-window launch
- * made with CGB_DEBUG_SW & 64 set (8 uint64 per CTA: total, wait accumulator,
- * wait A window, wait filter tile, tiles). Returns 0 on success. */
+/* Profiling hook (profiling builds, -DCGB_PROFILING; returns -1 otherwise): per-CTA
+ * MMA-issuer cycle counters of the last shifted-window launch made with debug & 64 set
+ * (16 uint64 per CTA: total, wait accumulator, wait A window, wait filter tile, tiles,
+ * epilogue wait/busy, timestamps). Returns 0 on success. */
 int cgb_debug_sw_stats(unsigned long long* host, int n_cta);
 
 #ifdef __cplusplus

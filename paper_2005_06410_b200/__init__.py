@@ -31,6 +31,7 @@ __all__ = [
     "conv", "conv_gemm", "conv_im2col_gemm", "convgemm_scratch_bytes", "empty_tensor4", "gemm_dims",
     "im2col", "im2col_workspace_bytes", "output_dims", "scratch_peak_bytes", "scratch_reset_peak",
     "scratch_set_limit", "kernel_launch_count", "last_path", "PRECISIONS", "ALGOS", "gemm",
+    "set_tuning", "get_tuning", "tuning",
     "IoError", "conv_workspace_bytes", "LayerSpec", "ModelSpec", "LayerResult", "ParseError", "UnknownLayerKind", "parse_model",
     "model_workspace_bytes", "run_inference", "write_csv",
 ]
@@ -166,6 +167,36 @@ def kernel_launch_count() -> int:
 
 def last_path() -> str:
     return PATHS.get(lib.cgb_last_path(), "?")
+
+
+def set_tuning(key: str, value: int) -> None:
+    """Dispatch-policy knob (include/convgemm_b200.h cgb_set_tuning); every setting is correct."""
+    _check(lib.cgb_set_tuning(key.encode(), int(value)))
+
+
+def get_tuning(key: str) -> int:
+    v = ctypes.c_int64()
+    _check(lib.cgb_get_tuning(key.encode(), ctypes.byref(v)))
+    return v.value
+
+
+class tuning:
+    """Context manager: ``with tuning(sk=2, tail=0): ...`` sets knobs and restores them."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_tuning(k)
+            set_tuning(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_tuning(k, v)
+        return False
 
 
 # ----------------------------------------------------------------------------- tensors

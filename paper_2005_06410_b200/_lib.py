@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("CGB_LIB_OVERRIDE") or os.path.join(HERE, "libconvgemm_b200.so")  # override: profiling
+# CGB_LIB_OVERRIDE: tools/ load the profiling build (libconvgemm_b200_prof.so) this way
+LIB_PATH = os.environ.get("CGB_LIB_OVERRIDE") or os.path.join(HERE, "libconvgemm_b200.so")
 
 # exported symbols, in include/convgemm_b200.h order
 SYMBOLS = (
@@ -18,7 +19,7 @@ SYMBOLS = (
     "cgb_conv_workspace_bytes", "cgb_conv", "cgb_conv_gemm", "cgb_conv_im2col_gemm", "cgb_im2col",
     "cgb_gemm", "cgb_conv_host", "cgb_scratch_current_bytes", "cgb_scratch_peak_bytes", "cgb_scratch_reset_peak",
     "cgb_scratch_set_limit", "cgb_scratch_release", "cgb_last_error", "cgb_version",
-    "cgb_kernel_launch_count", "cgb_last_path", "cgb_debug_sw_stats",
+    "cgb_kernel_launch_count", "cgb_last_path", "cgb_debug_sw_stats", "cgb_set_tuning", "cgb_get_tuning",
 )
 
 
@@ -63,6 +64,8 @@ def _load() -> ctypes.CDLL:
         "cgb_kernel_launch_count": (ctypes.c_uint64, []),
         "cgb_last_path": (ctypes.c_int, []),
         "cgb_debug_sw_stats": (ctypes.c_int, [vp, ctypes.c_int]),
+        "cgb_set_tuning": (st, [ctypes.c_char_p, i64]),
+        "cgb_get_tuning": (st, [ctypes.c_char_p, i64p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

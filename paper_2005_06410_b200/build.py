@@ -15,6 +15,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libconvgemm_b200.so")
+# profiling variant for tools/ (CGB_* environment knobs, CGB_DEBUG_SW stage switches and
+# per-CTA counters); never loaded by the package unless CGB_LIB_OVERRIDE points at it
+LIB_PROF = os.path.join(HERE, "libconvgemm_b200_prof.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -29,26 +32,27 @@ def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
     deps.append(os.path.join(os.path.dirname(HERE), "include", "convgemm_b200.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, *sources(), "-o", tmp]
+def build(force: bool = False, verbose: bool = False, profiling: bool = False) -> str:
+    lib = LIB_PROF if profiling else LIB
+    if not force and not stale(lib):
+        return lib
+    tmp = lib + ".tmp"
+    cmd = [NVCC, *FLAGS, *(["-DCGB_PROFILING"] if profiling else []), *sources(), "-o", tmp]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, profiling="--profiling" in sys.argv))

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "../../include/convgemm_b200.h"
 #include "internal.h"
@@ -47,6 +48,34 @@ bool can_free_now(cudaStream_t st) {
     return false;
   }
   return cs == cudaStreamCaptureStatusNone;
+}
+
+// ------------------------------------------------------------------ tuning
+static std::mutex g_tune_mu;
+static Tuning g_tune;
+
+#define CGB_TUNING_KEYS(X)                                                                                   \
+  X(sk) X(tail) X(pair) X(cfg) X(mt) X(bn) X(tma_a) X(tma_deep) X(pstore) X(pdl) X(verbose) X(smem_pad_kb) \
+  X(host_chunk_kb) X(host_no_bounce) X(host_copy_threads) X(debug)
+
+Tuning tuning() {
+  Tuning t;
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    t = g_tune;
+  }
+#ifdef CGB_PROFILING
+  auto env = [](const char* k, auto& v) {
+    if (const char* e = getenv(k)) v = (std::remove_reference_t<decltype(v)>)atoll(e);
+  };
+  env("CGB_SW_SK", t.sk); env("CGB_SW_TAIL", t.tail); env("CGB_SW_PAIR", t.pair); env("CGB_SW_CFG", t.cfg);
+  env("CGB_SW_MT", t.mt); env("CGB_SW_BN", t.bn); env("CGB_SW_TMA_A", t.tma_a); env("CGB_SW_TMA_DEEP", t.tma_deep);
+  env("CGB_SW_PSTORE", t.pstore); env("CGB_PDL", t.pdl); env("CGB_SW_VERBOSE", t.verbose);
+  env("CGB_SW_SMEM_PAD", t.smem_pad_kb); env("CGB_HOST_CHUNK_KB", t.host_chunk_kb);
+  env("CGB_HOST_NO_BOUNCE", t.host_no_bounce); env("CGB_HOST_COPY_THREADS", t.host_copy_threads);
+  env("CGB_DEBUG_SW", t.debug);
+#endif
+  return t;
 }
 
 static thread_local std::string g_last_error;
@@ -515,6 +544,32 @@ void cgb_scratch_release(void) {
   g_scratch.ptr = nullptr;
   g_scratch.bytes = 0;
   g_scratch.current.store(0);
+}
+
+cgb_status cgb_set_tuning(const char* key, int64_t value) {
+  if (!key) return fail(CGB_INVALID_ARGUMENT, "null tuning key");
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+#define CGB_SET(k)                                  \
+  if (strcmp(key, #k) == 0) {                       \
+    g_tune.k = (decltype(g_tune.k))value;           \
+    return CGB_OK;                                  \
+  }
+  CGB_TUNING_KEYS(CGB_SET)
+#undef CGB_SET
+  return fail(CGB_INVALID_ARGUMENT, std::string("unknown tuning key: ") + key);
+}
+
+cgb_status cgb_get_tuning(const char* key, int64_t* value) {
+  if (!key || !value) return fail(CGB_INVALID_ARGUMENT, "null tuning key or output");
+  const Tuning t = tuning();
+#define CGB_GET(k)                    \
+  if (strcmp(key, #k) == 0) {         \
+    *value = (int64_t)t.k;            \
+    return CGB_OK;                    \
+  }
+  CGB_TUNING_KEYS(CGB_GET)
+#undef CGB_GET
+  return fail(CGB_INVALID_ARGUMENT, std::string("unknown tuning key: ") + key);
 }
 
 const char* cgb_last_error(void) { return g_last_error.c_str(); }

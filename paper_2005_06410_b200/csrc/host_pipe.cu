@@ -82,8 +82,8 @@ class CopyPool {
   }
   CopyPool() {
     const int hw = (int)std::thread::hardware_concurrency();
-    const char* env = getenv("CGB_HOST_COPY_THREADS");
-    const int n = env ? atoi(env) : std::min(8, std::max(1, hw / 2));
+    const int req = tuning().host_copy_threads;
+    const int n = req > 0 ? req : std::min(8, std::max(1, hw / 2));
     for (int i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { run(); });
   }
   ~CopyPool() {
@@ -188,9 +188,7 @@ bool is_pinned(const void* p) {
 }  // namespace
 
 int64_t host_chunk_items(size_t in_item, size_t out_item, int64_t items) {
-  const char* env = getenv("CGB_HOST_CHUNK_MB");
-  const double mb = env ? atof(env) : 8.0;
-  const size_t target = (size_t)std::max(1.0, mb * 1048576.0);
+  const size_t target = (size_t)std::max<int64_t>(1, tuning().host_chunk_kb) * 1024;
   const size_t per = std::max<size_t>(1, std::max(in_item, out_item));
   int64_t c = (int64_t)std::max<size_t>(1, target / per);
   c = std::max<int64_t>(c, (items + 63) / 64);  // at most 64 chunks
@@ -212,8 +210,9 @@ static cudaError_t pipeline(DeviceState* d, const HostPipe& io, cudaStream_t com
   char* out_h = static_cast<char*>(io.out_host);
   char* in_d = static_cast<char*>(io.in_dev);
   const char* out_d = static_cast<const char*>(io.out_dev);
-  const bool direct_in = is_pinned(io.in_host) || getenv("CGB_HOST_NO_BOUNCE");
-  const bool direct_out = is_pinned(io.out_host) || getenv("CGB_HOST_NO_BOUNCE");
+  const bool no_bounce = tuning().host_no_bounce != 0;
+  const bool direct_in = is_pinned(io.in_host) || no_bounce;
+  const bool direct_out = is_pinned(io.out_host) || no_bounce;
 #define CGB_TRY(call, what)       \
   do {                            \
     if ((e = (call)) != cudaSuccess) { \

@@ -12,6 +12,32 @@
 
 namespace cgb {
 
+// Dispatch-policy knobs. Every setting is correct: they only choose among equivalent
+// kernel variants (tests force the rarer ones; tools sweep them). Set through
+// cgb_set_tuning(); the product library reads no environment variables. Profiling builds
+// (-DCGB_PROFILING, tools/) also take the CGB_* environment variables, read at every
+// launch, plus the correctness-breaking CGB_DEBUG_SW stage switches.
+struct Tuning {
+  int sk = 1;            // stream-K split of the last rounds: 0 never, 1 by fill, 2 whenever it fits
+  int tail = 1;          // tail tiles: 0 never, 1 by cost, 2 whenever they fit
+  int pair = 1;          // CTA pairs (cta_group::2) allowed
+  int cfg = -1;          // force one shifted-window candidate (index into kCands)
+  int mt = 0;            // force the M tile (subtiles of 128 rows)
+  int bn = 0;            // force the filter tile (64, 128, 256)
+  int tma_a = 1;         // TMA-fed A for 1x1 stride-1 layers
+  int tma_deep = 1;      // deep A rings for 1x1 layers
+  int pstore = 1;        // lane-pair epilogue stores
+  int pdl = 1;           // programmatic dependent launch
+  int verbose = 0;       // print the chosen configuration to stderr
+  int smem_pad_kb = 0;   // pad dynamic shared memory (shrinks the L1 carve-out)
+  int64_t host_chunk_kb = 8192;  // host path: chunk size of the H2D || conv || D2H pipeline
+  int host_no_bounce = 0;        // host path: DMA pageable buffers directly (no pinned ring)
+  int host_copy_threads = 0;     // host path: memcpy pool size (0 = min(8, cores/2))
+  int debug = 0;         // CGB_DEBUG_SW stage switches (profiling builds only)
+};
+// Snapshot of the current settings (profiling builds: overlaid with the environment).
+Tuning tuning();
+
 // Launch accounting (cgb_kernel_launch_count): every kernel launch site bumps it.
 void count_launch(uint64_t n = 1);
 

@@ -31,6 +31,13 @@
 
 #include "internal.h"
 
+// Profiling stage switches (CGB_DEBUG_SW, tools/ only): compiled out of the product.
+#ifdef CGB_PROFILING
+#define CGB_DBG(bit) ((a.dbg & (bit)) != 0)
+#else
+#define CGB_DBG(bit) (false)
+#endif
+
 namespace cgb {
 namespace sw {
 
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  if ((a.dbg & 64) && threadIdx.x == 0) {
+  if (CGB_DBG(64) && threadIdx.x == 0) {
     a.stats[blockIdx.x * 16 + 8] = gtimer();
     a.stats[blockIdx.x * 16 + 14] = smid();
   }
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       for (int s = 0; s < B_STAGES; ++s) {
         // TMA-skipping profile mode: both ranks arrive, so neither runs phases ahead
-        mbar_init(&b_full[s], (PAIR && (a.dbg & 8)) ? 2 : 1);
+        mbar_init(&b_full[s], (PAIR && CGB_DBG(8)) ? 2 : 1);
         mbar_init(&b_empty[s], 1);
       }
       for (int s = 0; s < 2; ++s) {
@@ -342,7 +349,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           // One unit in flight per iteration: a second one (the regular loop's UPI = 2)
           // raised the register pressure of the two-unit kernels for every layer.
           constexpr int WU = 1;
-          for (int u = warp; u < units && !(a.dbg & 1); u += WU * PRODUCER_WARPS) {
+          for (int u = warp; u < units && !CGB_DBG(1); u += WU * PRODUCER_WARPS) {
             float v[WU][BK];
             int32_t row[WU];
 #pragma unroll
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
         const int cmax = a.c_i - cc * BK;
         // UPI units in flight per iteration (UPI x 32 loads per thread)
-        for (int u = warp; u < units && !(a.dbg & 1); u += UPI * PRODUCER_WARPS) {
+        for (int u = warp; u < units && !CGB_DBG(1); u += UPI * PRODUCER_WARPS) {
           float v[UPI][BK];
           int32_t row[UPI];
           uint32_t off[UPI];
@@ -436,7 +443,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-    if ((a.dbg & 64) && warp == 0 && lane == 0) a.stats[blockIdx.x * 16 + 13] = gtimer();
+    if (CGB_DBG(64) && warp == 0 && lane == 0) a.stats[blockIdx.x * 16 + 13] = gtimer();
   } else if (warp == FWD_WARP) {
     // ---------------------------------------------------------------- window forwarder
     // A cluster-scope release arrive costs a GPU-wide memory barrier; paying it once per
@@ -487,7 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // ring is deep enough to hide the wake-up, and the spinning thread took issue
             // slots from the producer warps of its sub-partition (BN = 256 layers 0.5-1%).
             mbar_wait(&b_empty[bs], bph ^ 1);
-            if (a.dbg & 8) {
+            if (CGB_DBG(8)) {
               if (PAIR) mbar_arrive_cluster(lead_b_full + bs * 8);
               else mbar_arrive(&b_full[bs]);
             } else {
@@ -534,8 +541,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       int as = 0, bs = 0, t = 0;
       uint32_t aph = 0, bph = 0;
       unsigned long long w_t = 0, w_a = 0, w_b = 0, t_start = clock64();
-      if (a.dbg & 64) a.stats[blockIdx.x * 16 + 9] = gtimer();
-      const bool st = (a.dbg & 64) != 0;
+      if (CGB_DBG(64)) a.stats[blockIdx.x * 16 + 9] = gtimer();
+      const bool st = CGB_DBG(64);
       // K-major window (128-byte rows, k-step 32 B = 2 units) or, TMA-fed, MN-major 32-pixel
       // blocks like the filter tiles (k-step = 8 channel rows of 128 B = 64 units)
       const uint64_t a_desc0 = a.tma_a ? smem_desc(smem_u32(a_slot(0, 0)), 4096, 512, 0, kLayoutSW128_32B)
@@ -579,7 +586,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t at = a_hi0 + shift, at_lo = at + a_lo_off;
             const uint64_t bt = b_desc0 + (uint64_t)bs * b_stage_units, bt_lo = bt + b_lo_off;
             const uint32_t first = (cc == cc0 && tap == 0) ? 0u : 1u;
-            if (!(a.dbg & 2)) {
+            if (!CGB_DBG(2)) {
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk)
                 if (kk < a.ksteps)
@@ -611,7 +618,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                   }
             }
             if (PAIR) mma_commit_mc2(&b_empty[bs], 3);
-            else if (a.dbg & 32) mbar_arrive(&b_empty[bs]);
+            else if (CGB_DBG(32)) mbar_arrive(&b_empty[bs]);
             else mma_commit(&b_empty[bs]);
             if (++bs == B_STAGES) { bs = 0; bph ^= 1; }
           }
@@ -642,15 +649,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       int mtc;
       tile_rows<MT, PAIR>(a, tile, rank, m0, mtc);
       const int n0 = (tile / a.m_tiles) * BN;
-      unsigned long long e0 = (a.dbg & 64) ? clock64() : 0;
+      unsigned long long e0 = CGB_DBG(64) ? clock64() : 0;
       if (PAIR) {
         if (lane == 0) mbar_wait(&t_full[acc_set], acc_ph);
         __syncwarp();
       } else {
         mbar_wait_warp(&t_full[acc_set], acc_ph);
       }
-      unsigned long long e1 = (a.dbg & 64) ? clock64() : 0;
-      if (a.dbg & 64) epi_wait += e1 - e0;
+      unsigned long long e1 = CGB_DBG(64) ? clock64() : 0;
+      if (CGB_DBG(64)) epi_wait += e1 - e0;
       tc_fence_after();
       // ---- stream-K piece of a split tile. Groups' unit ranges are contiguous, so every
       // group whose range meets the tile holds exactly one piece of it, and the pieces are
@@ -677,7 +684,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
       }
 #pragma unroll 1
-      for (int mt = 0; mt < mtc && !(a.dbg & 16); ++mt) {
+      for (int mt = 0; mt < mtc && !CGB_DBG(16); ++mt) {
         const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
         int64_t P = -1;
         if (Q < a.Mp32) {
@@ -693,7 +700,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_ld_32x32b_x32(trow + cb * 32, r);
           tmem_ld_wait();
           const int nb = n0 + cb * 32;
-          if (a.pstore && a.vec && nb + 32 <= a.k_n && !(a.dbg & 4)) {
+          if (a.pstore && a.vec && nb + 32 <= a.k_n && !CGB_DBG(4)) {
             // Lane pairs write whole 64-byte runs: in store A_k the pair writes segments
             // 2k, 2k+1 (8 floats each) of the even lane's pixel, in B_k those of the odd
             // lane's pixel, after one shfl.xor exchange. Each warp store then touches 16
@@ -729,7 +736,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
               }
             }
-          } else if (P >= 0 && !(a.dbg & 4)) {
+          } else if (P >= 0 && !CGB_DBG(4)) {
             float* dst = O + P * a.k_n + nb;
             if (a.vec && nb + 32 <= a.k_n) {
               if (!add) {
@@ -765,9 +772,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (PAIR) mbar_arrive_cluster(lead_t_empty + acc_set * 8);
         else mbar_arrive(&t_empty[acc_set]);
       }
-      if (a.dbg & 64) epi_busy += clock64() - e1;
+      if (CGB_DBG(64)) epi_busy += clock64() - e1;
     }
-    if ((a.dbg & 64) && warp == EPI_WARP0 && lane == 0) {
+    if (CGB_DBG(64) && warp == EPI_WARP0 && lane == 0) {
       a.stats[blockIdx.x * 16 + 5] = epi_wait;
       a.stats[blockIdx.x * 16 + 6] = epi_busy;
       a.stats[blockIdx.x * 16 + 11] = gtimer();
@@ -776,7 +783,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_before();
   if (PAIR) cluster_sync();  // the leader's MMAs write the peer's TMEM: both must be done
   else __syncthreads();
-  if ((a.dbg & 64) && threadIdx.x == 0) a.stats[blockIdx.x * 16 + 12] = gtimer();
+  if (CGB_DBG(64) && threadIdx.x == 0) a.stats[blockIdx.x * 16 + 12] = gtimer();
   if (warp == TMA_WARP) {
     __syncwarp();
     tc_fence_after();
@@ -797,18 +804,6 @@ struct SkCounters {
 static std::mutex g_sk_mu;
 static std::map<std::pair<int, cudaStream_t>, SkCounters> g_sk;
 
-static bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("CGB_PDL");  // 0 = plain stream serialization
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
-}
-
-static int sk_env() {
-  const char* e = getenv("CGB_SW_SK");  // 0 = never split, 1 = auto (default), 2 = always
-  return e ? atoi(e) : 1;
-}
 
 static int* sk_counters(cudaStream_t st, size_t n) {
   std::lock_guard<std::mutex> lk(g_sk_mu);
@@ -829,7 +824,7 @@ static int* sk_counters(cudaStream_t st, size_t n) {
 
 template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR, int UPI>
 cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, Args a,
-                       cudaStream_t st) {
+                       cudaStream_t st, const Tuning& tu) {
   using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
   a.R = MT * 128 + a.dmax;
   a.R_pad = (a.R + 7) / 8 * 8;
@@ -842,8 +837,8 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   a.m_tiles = (int32_t)((a.Mp + pair_rows - 1) / pair_rows);
   a.n_tiles = (a.k_n + BN - 1) / BN;
   size_t smem = base_smem;
-  if (const char* pad = getenv("CGB_SW_SMEM_PAD"))  // profiling: shrink the L1 carve-out
-    smem = std::max<size_t>(smem, (size_t)atoi(pad) * 1024);
+  if (tu.smem_pad_kb > 0)  // profiling: shrink the L1 carve-out
+    smem = std::max<size_t>(smem, (size_t)tu.smem_pad_kb * 1024);
   auto kern = sw_conv_kernel<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR, UPI>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -857,8 +852,7 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   // rounds, the last half empty). Relative tile times as in the dispatcher's cost model.
   a.m_full = 0;
   a.tail_mt = 0;
-  const char* te = getenv("CGB_SW_TAIL");  // 0 = never, 2 = whenever it fits (tests), default: by cost
-  const int tail_mode = te ? atoi(te) : 1;
+  const int tail_mode = tu.tail;  // 0 = never, 2 = whenever it fits (tests), default: by cost
   if (a.n_tiles == 1 && MT >= 2 && tail_mode != 0) {
     auto tt = [](int mt) { return mt >= 4 ? 1.8 * mt / 4 : (mt == 2 ? 1.0 : 0.62); };
     const int64_t full_fit = a.Mp / pair_rows;
@@ -891,7 +885,7 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   a.counters = nullptr;
   const int rounds = (tiles + gmax - 1) / gmax;
   const double fill = (double)tiles / ((double)rounds * gmax);
-  const int sk_mode = sk_env();
+  const int sk_mode = tu.sk;
   // Stream-K only for the last one-to-two rounds of at least one tile per group: every
   // split tile adds a red.add pass over its rows (L2 atomics), which measured slower than
   // the idle SMs it saves when ALL tiles would be split (1-round layers: 7x7, 14x14).
@@ -906,7 +900,7 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
       a.sk_units = sk_tiles * a.CC;
     }
   }
-  if (getenv("CGB_SW_VERBOSE"))
+  if (tu.verbose)
     fprintf(stderr,
             "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d smem=%.1fKB tiles=%d (tail %d of mt %d) "
             "sk_units=%d\n",
@@ -926,7 +920,7 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (pdl_enabled()) {  // overlap this launch's setup with the tail of the previous grid
+  if (tu.pdl) {  // overlap this launch's setup with the tail of the previous grid
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
@@ -982,19 +976,20 @@ static Args make_args(const ConvGeom& g) {
   a.R = 0; a.m_tiles = 0; a.n_tiles = 0;
   a.m_full = 0; a.tail_mt = 0;
   a.ksteps = BK / 8;
-  const char* ps = getenv("CGB_SW_PSTORE");
-  a.pstore = ps ? atoi(ps) : 1;
+  a.pstore = tuning().pstore;
   a.wim = 0; a.wim_kw = 1; a.wim_ci = a.c_i;
   a.tma_a = 0;
-  const char* dbg = getenv("CGB_DEBUG_SW");
-  a.dbg = dbg ? atoi(dbg) : 0;
+  a.dbg = 0;
   a.stats = nullptr;
-  if (a.dbg & 64) {  // 8 launch slots of 1024 CTAs x 16 counters (slot = launch index % 8)
+#ifdef CGB_PROFILING
+  a.dbg = tuning().debug;
+  if (CGB_DBG(64)) {  // 8 launch slots of 1024 CTAs x 16 counters (slot = launch index % 8)
     if (!g_stats)
       capture_safe_malloc(reinterpret_cast<void**>(&g_stats), 8 * 1024 * 16 * sizeof(unsigned long long), true);
     static int slot = 0;
     a.stats = g_stats + (size_t)(slot++ % 8) * 1024 * 16;
   }
+#endif
   return a;
 }
 
@@ -1064,9 +1059,9 @@ constexpr int kFirstTmaACand = 48;   // deep A rings, tried first for 1x1 layers
 constexpr int kFirstProbeCand = 50;  // candidates from here on are CGB_SW_CFG probes only
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
-                               const Args& a, cudaStream_t st) {
+                               const Args& a, cudaStream_t st, const Tuning& tu) {
 #define CGB_SW_CASE(IDX, MT, BN, SP, AS, BS, PR, U) \
-  case IDX: return launch_cfg<MT, BN, SP, AS, BS, PR, U>(th, tl, I, O, a, st);
+  case IDX: return launch_cfg<MT, BN, SP, AS, BS, PR, U>(th, tl, I, O, a, st, tu);
   switch (i) {
     CGB_SW_CASE(0, 4, 64, false, 2, 8, true, 1)
     CGB_SW_CASE(1, 2, 64, false, 2, 8, true, 1)
@@ -1127,18 +1122,18 @@ static int bn_for(int k_n) { return k_n <= 64 ? 64 : (k_n <= 128 ? 128 : 256); }
 
 static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, const Args& a,
                             bool split, int sms, cudaStream_t st) {
+  const Tuning tu = tuning();
   int bn = bn_for(a.k_n);
-  if (const char* f = getenv("CGB_SW_BN")) bn = atoi(f);  // profiling override: 64, 128 or 256
+  if (tu.bn == 64 || tu.bn == 128 || tu.bn == 256) bn = tu.bn;  // forced filter tile
   const int n_tiles = (a.k_n + bn - 1) / bn;
-  if (const char* f = getenv("CGB_SW_CFG")) {  // profiling override: force one candidate
-    const int i = atoi(f);
-    if (i >= 0 && i < kNumCands && kCands[i].bn == bn && kCands[i].split == (int)split)
-      return launch_cand(i, th, tl, I, O, a, st);
+  if (tu.cfg >= 0) {  // forced candidate (when it matches the filter tile and precision)
+    const int i = tu.cfg;
+    if (i < kNumCands && kCands[i].bn == bn && kCands[i].split == (int)split)
+      return launch_cand(i, th, tl, I, O, a, st, tu);
   }
   // Preference (measured, tools/sweep_cfg.sh): CTA pairs first (CGB_SW_PAIR=0 disables),
   // then a double-buffered window (A slots = 2), then the M tile the cost model picks.
-  const char* pe = getenv("CGB_SW_PAIR");
-  const bool allow_pair = !(pe && atoi(pe) == 0);
+  const bool allow_pair = tu.pair != 0;
   // passes: pairs with a double-buffered window, pairs with any, single CTAs likewise
   for (int pass = 0; pass < 4; ++pass) {
     const int want_pair = pass < 2 ? 1 : 0;
@@ -1156,14 +1151,14 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
       const double tt = mt == 4 ? 1.8 : (mt == 2 ? 1.0 : 0.62);
       const int tiles = (int)((a.Mp + units * mt * 128 - 1) / (units * mt * 128)) * n_tiles;
       const int rounds = (tiles + gmax - 1) / gmax;
-      const bool sk = sk_env() != 0 && a.CC >= 2 && tiles >= gmax && (double)tiles / (rounds * gmax) < kSkFill;
+      const bool sk = tu.sk != 0 && a.CC >= 2 && tiles >= gmax && (double)tiles / (rounds * gmax) < kSkFill;
       const double cost = (sk ? (double)tiles / gmax * 1.03 : (double)rounds) * tt;
       if (cost < best * 0.98) {
         best = cost;
         mt_max = mt;
       }
     }
-    if (const char* f = getenv("CGB_SW_MT")) mt_max = atoi(f);  // profiling override
+    if (tu.mt > 0) mt_max = tu.mt;  // forced M tile
     // deep filter rings for the filter-stream-heavy layers: BN = 256 with several filter
     // tiles, or with a stride-1 (small) window that leaves the shared memory for them
     // (14x14 256->256: 62 -> 57 us); stride-2 windows keep the L1 instead
@@ -1181,10 +1176,9 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     int no = 0;
     if (split)
       for (int i = kFirstSplit2Cand; i < kFirstTmaACand; ++i) order[no++] = i;
-    const char* tdeep = getenv("CGB_SW_TMA_DEEP");  // A/B switch for the deep A rings
     // (staged 1x1 windows are as small -- no halo -- and gain too: 7x7 2048->512
     // 121 -> 100 us, 512->2048 96 -> 87 us)
-    if ((a.tma_a || (a.taps == 1 && !a.wim)) && !split && !(tdeep && atoi(tdeep) == 0))
+    if ((a.tma_a || (a.taps == 1 && !a.wim)) && !split && tu.tma_deep)
       for (int i = kFirstTmaACand; i < kFirstProbeCand; ++i) order[no++] = i;
     if (upi2)
       for (int i = kFirstUpi2Cand; i < kFirstSplit2Cand; ++i) order[no++] = i;
@@ -1200,9 +1194,9 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
                           (a.Mp + 511) / 512 * n_tiles >= (want_pair ? sms / 2 : sms) / 2;
       if (c.bn != bn || c.split != (int)split || (c.mt > mt_max && !deep_a) || c.pair != want_pair) continue;
       if (pass % 2 == 0 && c.as < 2) continue;
-      cudaError_t e = launch_cand(i, th, tl, I, O, a, st);
+      cudaError_t e = launch_cand(i, th, tl, I, O, a, st, tu);
       if (e != cudaErrorNotSupported) {
-        if (getenv("CGB_SW_VERBOSE"))
+        if (tu.verbose)
           fprintf(stderr, "[cgb] shifted cand %d: MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d\n", i, c.mt, c.bn,
                   c.split, c.as, c.bs, c.pair, c.upi);
         return e;
@@ -1230,10 +1224,9 @@ cudaError_t launch_tc_conv_shifted(const float* f_hi, const float* f_lo, int64_t
   // channel plane, i.e. MN-major), no producer staging. Needs 16-byte channel-plane
   // strides (h*w % 4 == 0) and a 16-byte aligned I; rows are the pixels of each image
   // padded to a multiple of 32 (the TMA box), so the plane is (hw32 x 1) per image.
-  const char* te = getenv("CGB_SW_TMA_A");
   const int64_t hw = g.h_i * g.w_i;
   if (!split && g.k_h == 1 && g.k_w == 1 && g.s == 1 && g.p == 0 && hw % 4 == 0 &&
-      reinterpret_cast<uintptr_t>(I) % 16 == 0 && !(te && atoi(te) == 0)) {
+      reinterpret_cast<uintptr_t>(I) % 16 == 0 && tuning().tma_a) {
     const int64_t hwp = (hw + 31) / 32 * 32;
     if ((hwp * g.b) < (int64_t(1) << 30) && make_input_tmap_1x1(&tl, I, g) == cudaSuccess) {
       a.tma_a = 1;
@@ -1313,6 +1306,11 @@ cudaError_t launch_tc_conv_wim(const float* f_hi, const float* f_lo, const float
 // MMA loop start, MMA loop end, epilogue end, exit, producers end; and the SM id.
 extern "C" int cgb_debug_sw_stats(unsigned long long* host, int n_cta) {
   // n_cta > 1024: all 8 launch slots (8 x 1024 x 16 counters); host == NULL: zero them
+#ifndef CGB_PROFILING
+  (void)host;
+  (void)n_cta;
+  return -1;
+#endif
   if (!cgb::sw::g_stats) return -1;
   const size_t n = n_cta > 1024 ? (size_t)8 * 1024 * 16 : (size_t)n_cta * 16;
   if (!host) return cudaMemset(cgb::sw::g_stats, 0, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;

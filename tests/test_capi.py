@@ -98,3 +98,22 @@ def test_low_channel_workspace():
     stem = (64, 7, 7, 3, 224, 224, 256, 2, 3)
     assert cg.conv_workspace_bytes(stem, "fused", "tf32") >= 64 * 7 * 32 * 4
     assert cg.conv_workspace_bytes(stem, "fused", "3xtf32") >= 2 * 64 * 7 * 32 * 4
+
+
+def test_tuning_knobs_roundtrip_and_no_env():
+    """Dispatch-policy knobs go through cgb_set_tuning (the product reads no environment
+    variables); unknown keys are rejected with the reference's invalid_argument status."""
+    import os
+    assert cg.get_tuning("sk") == 1
+    with cg.tuning(sk=2, tail=0, host_chunk_kb=20):
+        assert (cg.get_tuning("sk"), cg.get_tuning("tail"), cg.get_tuning("host_chunk_kb")) == (2, 0, 20)
+    assert (cg.get_tuning("sk"), cg.get_tuning("tail")) == (1, 1)
+    with pytest.raises(ValueError):
+        cg.set_tuning("no_such_knob", 1)
+    os.environ["CGB_SW_SK"] = "2"
+    try:
+        assert cg.get_tuning("sk") == 1  # the product library ignores the environment
+    finally:
+        del os.environ["CGB_SW_SK"]
+    strings = open(cg._lib.LIB_PATH, "rb").read()
+    assert b"CGB_DEBUG_SW" not in strings and b"CGB_SW_SK" not in strings

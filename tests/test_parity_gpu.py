@@ -191,18 +191,15 @@ def _pinned_fortran(a):
     return v.reshape(a.shape, order="F"), t
 
 
-@pytest.mark.parametrize("chunk_mb", ["0.02", "0.07", "1000"])
+@pytest.mark.parametrize("chunk_kb", [20, 70, 1 << 20])
 @pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("bounce", [True, False])
-def test_host_pipeline_chunking(monkeypatch, chunk_mb, pinned, bounce):
+def test_host_pipeline_chunking(chunk_kb, pinned, bounce):
     """cgb_conv_host cuts the batch into chunks (H2D || conv || D2H on three streams,
     pinned bounce ring for pageable buffers). Any chunking -- one chunk, more chunks
     than bounce slots, a ragged last chunk -- gives the device-path result bit for bit."""
     cp = dict(k_n=32, k_h=3, k_w=3, c_i=16, h_i=21, w_i=19, b=11, s=2, p=1)
     F, I = rand_inputs(cp, 12)
-    monkeypatch.setenv("CGB_HOST_CHUNK_MB", chunk_mb)  # 0.02 MB -> 1 image per chunk
-    if not bounce:
-        monkeypatch.setenv("CGB_HOST_NO_BOUNCE", "1")
     keep = []
     if pinned:
         F, kf = _pinned_fortran(F)
@@ -210,12 +207,14 @@ def test_host_pipeline_chunking(monkeypatch, chunk_mb, pinned, bounce):
         keep += [kf, ki]
     for prec in ("3xtf32", "tf32"):
         dev = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo="fused", precision=prec))
-        host = cg.conv(F, I, cp, algo="fused", precision=prec)
-        assert np.array_equal(host, dev), (chunk_mb, pinned, bounce, prec)
-        if pinned:
-            ho, kt = _pinned_fortran(np.zeros_like(host))
-            cg.conv(F, I, cp, algo="fused", precision=prec, out=ho)
-            assert np.array_equal(ho, dev)
+        # 20 KB -> 1 image per chunk
+        with cg.tuning(host_chunk_kb=chunk_kb, host_no_bounce=0 if bounce else 1):
+            host = cg.conv(F, I, cp, algo="fused", precision=prec)
+            assert np.array_equal(host, dev), (chunk_kb, pinned, bounce, prec)
+            if pinned:
+                ho, kt = _pinned_fortran(np.zeros_like(host))
+                cg.conv(F, I, cp, algo="fused", precision=prec, out=ho)
+                assert np.array_equal(ho, dev)
 
 
 def test_reference_named_entry_points(orc):
@@ -313,15 +312,15 @@ VARIANT_CASES = [
     dict(k_n=96, k_h=1, k_w=1, c_i=40, h_i=10, w_i=10, b=5, s=1, p=0),
     dict(k_n=512, k_h=1, k_w=1, c_i=1024, h_i=14, w_i=14, b=2, s=1, p=0),
 ])
-def test_tma_fed_1x1_bitwise_equal_to_staged(monkeypatch, cp):
+def test_tma_fed_1x1_bitwise_equal_to_staged(cp):
     # TF32 1x1: the TMA-fed A tile (MN-major, straight from I) and the producer-staged
     # K-major window feed the same fp32 bits to the same UMMAs in the same order
     F, I = rand_inputs(cp, 4242)
     Fd, Id = to_dev(F), to_dev(I)
-    monkeypatch.setenv("CGB_SW_TMA_A", "0")
-    staged = to_host(cg.conv(Fd, Id, cp, algo="fused", precision="tf32"))
-    monkeypatch.setenv("CGB_SW_TMA_A", "1")
-    tma = to_host(cg.conv(Fd, Id, cp, algo="fused", precision="tf32"))
+    with cg.tuning(tma_a=0):
+        staged = to_host(cg.conv(Fd, Id, cp, algo="fused", precision="tf32"))
+    with cg.tuning(tma_a=1):
+        tma = to_host(cg.conv(Fd, Id, cp, algo="fused", precision="tf32"))
     assert cg.last_path() == "tcgen05-shifted"
     assert np.array_equal(staged.view(np.uint32), tma.view(np.uint32))
 
@@ -348,7 +347,7 @@ SK_CASES = [
     dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=28, w_i=28, b=24, s=1, p=1),
     dict(k_n=128, k_h=3, k_w=3, c_i=64, h_i=56, w_i=56, b=24, s=2, p=1),
     dict(k_n=96, k_h=3, k_w=3, c_i=80, h_i=20, w_i=20, b=48, s=1, p=1),
-    # fewer tiles than SM pairs, many channel chunks, stream-K forced (CGB_SW_SK=2): every
+    # fewer tiles than SM pairs, many channel chunks, stream-K forced (tuning sk=2): every
     # tile is split into several pieces, combined in the fixed highest-chunk-first order
     dict(k_n=256, k_h=3, k_w=3, c_i=512, h_i=7, w_i=7, b=48, s=1, p=1, force=True),
     dict(k_n=512, k_h=3, k_w=3, c_i=256, h_i=14, w_i=14, b=48, s=2, p=1, force=True),
@@ -357,21 +356,21 @@ SK_CASES = [
 
 @pytest.mark.parametrize("case", range(len(SK_CASES)))
 @pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
-def test_stream_k(orc, monkeypatch, case, prec):
+def test_stream_k(orc, case, prec):
     cp = dict(SK_CASES[case])
-    if cp.pop("force", False):
-        monkeypatch.setenv("CGB_SW_SK", "2")
+    sk = 2 if cp.pop("force", False) else 1
     F, I = rand_inputs(cp, 300 + case)
     ref = orc.conv_gemm(F, I, cp)
     scale = orc.output_scale(F, I, cp)
     dF, dI = to_dev(F), to_dev(I)
-    a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
-    assert cg.last_path() in ("tcgen05-shifted", "tcgen05-gather"), cg.last_path()
-    b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    with cg.tuning(sk=sk):
+        a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+        assert cg.last_path() in ("tcgen05-shifted", "tcgen05-gather"), cg.last_path()
+        b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
     assert np.array_equal(a, b), "stream-K result must not depend on which piece finishes first"
     assert per_output_error(a, ref, scale) <= TOL[prec]
-    monkeypatch.setenv("CGB_SW_SK", "0")
-    whole = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    with cg.tuning(sk=0):
+        whole = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
     assert per_output_error(whole, ref, scale) <= TOL[prec]
     if cg.last_path() == "tcgen05-shifted":
         # the split changes the fp32 summation order of the split tiles: proof it engaged
@@ -380,7 +379,7 @@ def test_stream_k(orc, monkeypatch, case, prec):
 
 # ---------------------------------------------------------------- tail tiles
 TAIL_CASES = [
-    # forced (CGB_SW_TAIL=2): whole 4-subtile pair tiles for one round, then 2-subtile
+    # forced (tuning tail=2): whole 4-subtile pair tiles for one round, then 2-subtile
     # (or 1-subtile) tail tiles for the remaining rows
     dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=56, w_i=56, b=26, s=1, p=1),
     dict(k_n=128, k_h=3, k_w=3, c_i=32, h_i=28, w_i=28, b=70, s=1, p=1),
@@ -390,17 +389,17 @@ TAIL_CASES = [
 
 @pytest.mark.parametrize("case", range(len(TAIL_CASES)))
 @pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
-def test_tail_tiles(orc, monkeypatch, case, prec):
+def test_tail_tiles(orc, case, prec):
     cp = TAIL_CASES[case]
     F, I = rand_inputs(cp, 500 + case)
     ref = orc.conv_gemm(F, I, cp)
     scale = orc.output_scale(F, I, cp)
     dF, dI = to_dev(F), to_dev(I)
-    monkeypatch.setenv("CGB_SW_TAIL", "2")
-    a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    with cg.tuning(tail=2):
+        a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
     assert per_output_error(a, ref, scale) <= TOL[prec]
-    monkeypatch.setenv("CGB_SW_TAIL", "0")
-    b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    with cg.tuning(tail=0):
+        b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
     assert per_output_error(b, ref, scale) <= TOL[prec]
     if cg.last_path() == "tcgen05-shifted":
         # whole tiles in both launches (no stream-K split): the same bits either way

@@ -23,6 +23,8 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _prof  # noqa: E402,F401  (profiling build: CGB_* env knobs)
 import paper_2005_06410_b200 as cg  # noqa: E402
 
 

@@ -6,6 +6,8 @@ os.environ["CGB_DEBUG_SW"] = "64"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _prof  # noqa: E402,F401  (profiling build: CGB_* env knobs)
 import paper_2005_06410_b200 as cg
 import bench
 tensors = bench.make_layer_tensors(cg, torch, bench.LAYERS, 128, 0, 1)

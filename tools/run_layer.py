@@ -5,6 +5,8 @@ overhead hidden behind device execution), after `warm` warm-up launches."""
 import argparse, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _prof  # noqa: E402,F401  (profiling build: CGB_* env knobs)
 import paper_2005_06410_b200 as cg
 import bench
 

@@ -7,6 +7,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _prof  # noqa: E402,F401  (profiling build: CGB_* env knobs)
 import paper_2005_06410_b200 as cg  # noqa: E402
 from paper_2005_06410_b200 import models  # noqa: E402
 

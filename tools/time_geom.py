@@ -6,6 +6,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _prof  # noqa: E402,F401  (profiling build: CGB_* env knobs)
 import paper_2005_06410_b200 as cg  # noqa: E402
 
 k_n, k, c_i, h, s, p, b = map(int, sys.argv[1:8])
