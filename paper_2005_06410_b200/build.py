@@ -46,9 +46,25 @@ def build(force: bool = False, verbose: bool = False, profiling: bool = False) -
     if not force and not stale(lib):
         return lib
     tmp = lib + ".tmp"
-    cmd = [NVCC, *FLAGS, *(["-DCGB_PROFILING"] if profiling else []), *sources(), "-o", tmp]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
+    extra = ["-DCGB_PROFILING"] if profiling else []
+    # one nvcc per translation unit in parallel (the shifted-window kernel instantiates
+    # ~50 configurations), then one device-aware link
+    objdir = os.path.join(HERE, "build", "prof" if profiling else "rel")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *compile_flags, *extra, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp]
     subprocess.run(cmd, check=True)
     os.replace(tmp, lib)
     return lib

@@ -188,6 +188,80 @@ struct Cfg {
   static_assert(BN % 64 == 0, "epilogue works in 64-column blocks");
 };
 
+// The UMMAs of one tap: K = 4 k-steps of 8 x (BN / UMMA_N) N halves x MT M subtiles
+// (3 per product for 3xTF32: lo*hi + hi*lo + hi*hi). Fully unrolled with compile-time
+// descriptor offsets and no branches: the single issuing thread must keep up with N = 64
+// UMMAs (~43 cycles each), so its per-UMMA instruction count matters (tools/pair_bench.cu).
+// Descriptor units are 16 bytes: A m-subtile 128 rows = 1024, A k-step a_kstep (K-major
+// window: 2; MN-major TMA-fed tile: 64), B k-step 8 rows of 128 B = 64, B 32-filter block
+// 4096 B = 256.
+template <int MT, int BN, bool SPLIT, bool PAIR, int KS>
+CGB_DEV void issue_tap(uint32_t d_base, uint64_t at, uint64_t at_lo, uint64_t bt, uint64_t bt_lo, uint32_t idesc,
+                       uint32_t a_kstep, uint32_t first) {
+  constexpr int UN = BN > 256 ? 256 : BN;
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+    for (int hf = 0; hf < BN / UN; ++hf)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const uint64_t ad = at + (uint64_t)(mt * 1024) + (uint64_t)kk * a_kstep;
+        const uint64_t bd = bt + (uint64_t)(hf * (UN / 32) * 256 + kk * 64);
+        const uint32_t d = d_base + (uint32_t)(mt * BN + hf * UN);
+        const uint32_t acc = kk == 0 ? first : 1u;
+        if (SPLIT) {
+          const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024) + (uint64_t)kk * a_kstep;
+          const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (UN / 32) * 256 + kk * 64);
+          if (PAIR) {
+            mma_tf32_2cta(d, ad_lo, bd, idesc, acc);
+            mma_tf32_2cta(d, ad, bd_lo, idesc, 1);
+            mma_tf32_2cta(d, ad, bd, idesc, 1);
+          } else {
+            mma_tf32(d, ad_lo, bd, idesc, acc);
+            mma_tf32(d, ad, bd_lo, idesc, 1);
+            mma_tf32(d, ad, bd, idesc, 1);
+          }
+        } else {
+          if (PAIR) mma_tf32_2cta(d, ad, bd, idesc, acc);
+          else mma_tf32(d, ad, bd, idesc, acc);
+        }
+      }
+}
+
+// Tail tiles (mtc < MT subtiles) and w-im2col rows (ks < 4 k-steps): runtime bounds.
+template <int MT, int BN, bool SPLIT, bool PAIR>
+CGB_DEV void issue_tap_partial(uint32_t d_base, uint64_t at, uint64_t at_lo, uint64_t bt, uint64_t bt_lo,
+                               uint32_t idesc, uint32_t a_kstep, uint32_t first, int mtc, int ks) {
+  constexpr int UN = BN > 256 ? 256 : BN;
+#pragma unroll 1
+  for (int kk = 0; kk < ks; ++kk)
+#pragma unroll
+    for (int hf = 0; hf < BN / UN; ++hf)
+#pragma unroll 1
+      for (int mt = 0; mt < mtc; ++mt) {
+        const uint64_t ad = at + (uint64_t)(mt * 1024) + (uint64_t)kk * a_kstep;
+        const uint64_t bd = bt + (uint64_t)(hf * (UN / 32) * 256 + kk * 64);
+        const uint32_t d = d_base + (uint32_t)(mt * BN + hf * UN);
+        const uint32_t acc = kk == 0 ? first : 1u;
+        if (SPLIT) {
+          const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024) + (uint64_t)kk * a_kstep;
+          const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (UN / 32) * 256 + kk * 64);
+          if (PAIR) {
+            mma_tf32_2cta(d, ad_lo, bd, idesc, acc);
+            mma_tf32_2cta(d, ad, bd_lo, idesc, 1);
+            mma_tf32_2cta(d, ad, bd, idesc, 1);
+          } else {
+            mma_tf32(d, ad_lo, bd, idesc, acc);
+            mma_tf32(d, ad, bd_lo, idesc, 1);
+            mma_tf32(d, ad, bd, idesc, 1);
+          }
+        } else {
+          if (PAIR) mma_tf32_2cta(d, ad, bd, idesc, acc);
+          else mma_tf32(d, ad, bd, idesc, acc);
+        }
+      }
+}
+
 // PAIR = true: launched as clusters of 2 CTAs (a TPC); the leader (rank 0) issues
 // tcgen05.mma.cta_group::2 with M = 256 -- A rows 0-127 from the leader's window, 128-255
 // from the peer's window at the same shared-memory offset, B split into two halves of
@@ -553,6 +627,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t b_desc0 = smem_desc(smem_u32(b_slot(0, 0)), 4096, 512, 0, kLayoutSW128_32B);
       constexpr uint64_t b_lo_off = SPLIT ? (uint64_t)(C::B_TILE >> 4) : 0;
       constexpr uint64_t b_stage_units = (uint64_t)(C::NS * C::B_TILE) >> 4;
+      const bool full_steps = a.ksteps == BK / 8;  // every k-step issued (all but w-im2col rows)
       int tile, cc0, cc1;
       for (; seg_get(a, gid, t, tile, cc0, cc1); ++t) {
         const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
@@ -587,35 +662,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t bt = b_desc0 + (uint64_t)bs * b_stage_units, bt_lo = bt + b_lo_off;
             const uint32_t first = (cc == cc0 && tap == 0) ? 0u : 1u;
             if (!CGB_DBG(2)) {
-#pragma unroll
-              for (int kk = 0; kk < BK / 8; ++kk)
-                if (kk < a.ksteps)
-#pragma unroll
-                for (int hf = 0; hf < BN / C::UMMA_N; ++hf)
-#pragma unroll
-                  for (int mt = 0; mt < MT; ++mt) {
-                    if (mt >= mtc) break;  // tail tile: fewer M subtiles
-                    const uint64_t ad = at + (uint64_t)(mt * 1024 + kk * a_kstep);
-                    const uint64_t bd = bt + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
-                    const uint32_t d = d_base + mt * BN + hf * C::UMMA_N;
-                    const uint32_t acc = kk == 0 ? first : 1u;
-                    if (SPLIT) {
-                      const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024 + kk * a_kstep);
-                      const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (C::UMMA_N / 32) * 256 + kk * 64);
-                      if (PAIR) {
-                        mma_tf32_2cta(d, ad_lo, bd, idesc, acc);
-                        mma_tf32_2cta(d, ad, bd_lo, idesc, 1);
-                        mma_tf32_2cta(d, ad, bd, idesc, 1);
-                      } else {
-                        mma_tf32(d, ad_lo, bd, idesc, acc);
-                        mma_tf32(d, ad, bd_lo, idesc, 1);
-                        mma_tf32(d, ad, bd, idesc, 1);
-                      }
-                    } else {
-                      if (PAIR) mma_tf32_2cta(d, ad, bd, idesc, acc);
-                      else mma_tf32(d, ad, bd, idesc, acc);
-                    }
-                  }
+              if (full_steps && mtc == MT)
+                issue_tap<MT, BN, SPLIT, PAIR, BK / 8>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first);
+              else
+                issue_tap_partial<MT, BN, SPLIT, PAIR>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first, mtc,
+                                                       a.ksteps);
             }
             if (PAIR) mma_commit_mc2(&b_empty[bs], 3);
             else if (CGB_DBG(32)) mbar_arrive(&b_empty[bs]);
