@@ -83,6 +83,7 @@ struct Args {
   int* counters;      // [sk tile][ranks*4 epilogue warps] pieces written; zero between launches
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
+  int32_t tps;        // taps per filter stage group (divides B_STAGES; see the filter TMA warp)
   int32_t pstore;     // epilogue stores: 1 lane pairs 64 B (default), 0 per-lane 32 B (CGB_SW_PSTORE=0)
   int32_t tma_a;      // 1x1 layers: A (pixels x channels) TMA'd MN-major straight from I, no staging
   int32_t wim;        // w-im2col mode: a row holds the k_w*c_i values of one output row's w-taps
@@ -535,8 +536,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------------- filter TMA
     if (elect_one()) {
       constexpr uint32_t bytes = C::NS * C::B_TILE * (PAIR ? 2 : 1);  // both halves signal the leader
-      int bs = 0;
-      uint32_t bph = 0;
+      const int G = a.tps, NG = B_STAGES / a.tps;  // taps per filter stage group, groups in the ring
+      int bs = 0, gq = 0, gb = 0;                    // ring slot, position in its group, group
+      uint32_t gph = 0;
+      // group complete: the leader's arrive (G > 1: after the group's expect_tx; TMA-less
+      // profiling mode: both CTAs arrive)
+      auto close_group = [&](int g) {
+        if (CGB_DBG(8)) {
+          if (PAIR) mbar_arrive_cluster(lead_b_full + g * 8);
+          else mbar_arrive(&b_full[g]);
+        } else if (G > 1 && rank == 0) {
+          mbar_arrive(&b_full[g]);
+        }
+      };
       const uint32_t b0_hi = smem_u32(b_slot(0, 0)), b0_lo = smem_u32(b_slot(0, SPLIT ? 1 : 0));
       int tile, cc0, cc1;
       int ait = 0;  // TMA-fed A: chunk counter (window slot ring)
@@ -567,31 +579,40 @@ __global__ void __launch_bounds__(THREADS, 1)
             // WAR on own smem: CTA scope suffices. A suspending try_wait, not a spin: the
             // ring is deep enough to hide the wake-up, and the spinning thread took issue
             // slots from the producer warps of its sub-partition (BN = 256 layers 0.5-1%).
-            mbar_wait(&b_empty[bs], bph ^ 1);
-            if (CGB_DBG(8)) {
-              if (PAIR) mbar_arrive_cluster(lead_b_full + bs * 8);
-              else mbar_arrive(&b_full[bs]);
-            } else {
-              if (rank == 0) mbar_arrive_expect_tx(&b_full[bs], bytes);
+            // Filter stages are handed over in groups of G taps (one wait, one arrive, one
+            // commit per group): a hand-over costs the pair ~270-340 cycles
+            // (tools/pair_bench.cu), more than one tap of UMMAs for MT = 1, BN <= 128.
+            if (gq == 0) mbar_wait(&b_empty[gb], gph ^ 1);
+            if (!CGB_DBG(8)) {
+              if (rank == 0) {
+                if (G == 1) mbar_arrive_expect_tx(&b_full[gb], bytes);
+                else mbar_expect_tx(&b_full[gb], bytes);
+              }
               const uint32_t stage_off = (uint32_t)bs * C::NS * C::B_TILE;
 #pragma unroll
               for (int j = 0; j < C::NB / 32; ++j) {
                 if (PAIR) {
-                  tma_load_3d_2sm(b0_hi + stage_off + j * 4096, &tmap_hi, lead_b_full + bs * 8, n0 + 32 * j, tap,
+                  tma_load_3d_2sm(b0_hi + stage_off + j * 4096, &tmap_hi, lead_b_full + gb * 8, n0 + 32 * j, tap,
                                   cc * BK);
                   if (SPLIT)
-                    tma_load_3d_2sm(b0_lo + stage_off + j * 4096, &tmap_lo, lead_b_full + bs * 8, n0 + 32 * j, tap,
+                    tma_load_3d_2sm(b0_lo + stage_off + j * 4096, &tmap_lo, lead_b_full + gb * 8, n0 + 32 * j, tap,
                                     cc * BK);
                 } else {
-                  tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[bs], n0 + 32 * j, tap, cc * BK);
-                  if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[bs], n0 + 32 * j, tap, cc * BK);
+                  tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[gb], n0 + 32 * j, tap, cc * BK);
+                  if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[gb], n0 + 32 * j, tap, cc * BK);
                 }
               }
             }
-            if (++bs == B_STAGES) { bs = 0; bph ^= 1; }
+            if (gq == G - 1) close_group(gb);
+            if (++bs == B_STAGES) bs = 0;
+            if (++gq == G) {
+              gq = 0;
+              if (++gb == NG) { gb = 0; gph ^= 1; }
+            }
           }
         }
       }
+      if (gq != 0) close_group(gb);  // a last, partial group
     }
   } else if (warp == MMA_WARP) {
     // ---------------------------------------------------------------- MMA issue
@@ -613,7 +634,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       // m-subtile 128 rows = 1024 units, B k-step 1024 B = 64 units, 32-filter block
       // 4096 B = 256 units), so each issue is an add on a uniform register.
       int as = 0, bs = 0, t = 0;
-      uint32_t aph = 0, bph = 0;
+      uint32_t aph = 0;
+      const int G = a.tps, NG = B_STAGES / a.tps;  // filter stage groups (see the TMA warp)
+      int gq = 0, gb = 0;
+      uint32_t gph = 0;
       unsigned long long w_t = 0, w_a = 0, w_b = 0, t_start = clock64();
       if (CGB_DBG(64)) a.stats[blockIdx.x * 16 + 9] = gtimer();
       const bool st = CGB_DBG(64);
@@ -655,9 +679,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             unsigned long long c2 = st ? clock64() : 0;
             // TMA completion bytes of both halves land on this (leader's) barrier; the
             // UMMA reads the data through the async proxy, so a CTA-scope wait suffices.
-            mbar_wait_spin(&b_full[bs], bph);
+            if (gq == 0) {
+              mbar_wait_spin(&b_full[gb], gph);
+              tc_fence_after();
+            }
             if (st) w_b += clock64() - c2;
-            tc_fence_after();
             const uint64_t at = a_hi0 + shift, at_lo = at + a_lo_off;
             const uint64_t bt = b_desc0 + (uint64_t)bs * b_stage_units, bt_lo = bt + b_lo_off;
             const uint32_t first = (cc == cc0 && tap == 0) ? 0u : 1u;
@@ -668,10 +694,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                 issue_tap_partial<MT, BN, SPLIT, PAIR>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first, mtc,
                                                        a.ksteps);
             }
-            if (PAIR) mma_commit_mc2(&b_empty[bs], 3);
-            else if (CGB_DBG(32)) mbar_arrive(&b_empty[bs]);
-            else mma_commit(&b_empty[bs]);
-            if (++bs == B_STAGES) { bs = 0; bph ^= 1; }
+            if (gq == G - 1) {
+              if (PAIR) mma_commit_mc2(&b_empty[gb], 3);
+              else mma_commit(&b_empty[gb]);
+            }
+            if (++bs == B_STAGES) bs = 0;
+            if (++gq == G) {
+              gq = 0;
+              if (++gb == NG) { gb = 0; gph ^= 1; }
+            }
           }
           if (PAIR) mma_commit_mc2(&a_empty[as], 3);
           else mma_commit(&a_empty[as]);
@@ -879,6 +910,27 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   using C = Cfg<MT, BN, SPLIT, A_SLOTS, B_STAGES, PAIR>;
   a.R = MT * 128 + a.dmax;
   a.R_pad = (a.R + 7) / 8 * 8;
+  // Filter stages per hand-over: enough taps that one group's UMMAs (~BN/2 cycles per
+  // 128-row UMMA and k-step, x3 for 3xTF32) outlast a hand-over (~400 cycles measured),
+  // keeping at least two groups in the ring.
+  {
+    const int tap_cycles = MT * a.ksteps * (BN / 2) * (SPLIT ? 3 : 1);
+    int g = 1;
+    if (tu.tps > 0) {
+      g = tu.tps;
+    } else {
+      while (g * tap_cycles < 400 && B_STAGES % (g + 1) == 0 && B_STAGES / (g + 1) >= 2) ++g;
+      if (g * tap_cycles < 400)  // the next divisor of the ring (e.g. 3 of 6 after 2 failed)
+        for (int h = g + 1; h <= B_STAGES / 2; ++h)
+          if (B_STAGES % h == 0) { g = h; break; }
+    }
+    // TMA-fed A: the filter warp also loads A, one chunk (one tap) at a time, before each
+    // chunk's filter tap; closing a group of G chunks needs A slots for all of them while
+    // the MMAs still wait for that group: G <= A_SLOTS, or the two rings deadlock.
+    if (a.tma_a && g > A_SLOTS) g = A_SLOTS;
+    if (g < 1 || B_STAGES % g != 0 || (g > 1 && B_STAGES / g < 2)) g = 1;
+    a.tps = g;
+  }
   fast_div_magic((uint32_t)(a.Hq * a.Wq), a.fd_hwq_m, a.fd_hwq_p);
   fast_div_magic((uint32_t)a.Hq, a.fd_hq_m, a.fd_hq_p);
   const uint32_t a_slot_bytes = (uint32_t)(a.NPH * a.R_pad * 128);
@@ -953,9 +1005,9 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   }
   if (tu.verbose)
     fprintf(stderr,
-            "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d smem=%.1fKB tiles=%d (tail %d of mt %d) "
-            "sk_units=%d\n",
-            MT, BN, (int)SPLIT, A_SLOTS, B_STAGES, (int)PAIR, UPI, smem / 1024.0, tiles,
+            "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d tps=%d smem=%.1fKB tiles=%d (tail %d of mt "
+            "%d) sk_units=%d\n",
+            MT, BN, (int)SPLIT, A_SLOTS, B_STAGES, (int)PAIR, UPI, a.tps, smem / 1024.0, tiles,
             a.tail_mt ? a.m_tiles - a.m_full : 0, a.tail_mt, a.sk_units);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((PAIR ? 2 : 1) * a.groups));
@@ -1027,6 +1079,7 @@ static Args make_args(const ConvGeom& g) {
   a.R = 0; a.m_tiles = 0; a.n_tiles = 0;
   a.m_full = 0; a.tail_mt = 0;
   a.ksteps = BK / 8;
+  a.tps = 1;
   a.pstore = tuning().pstore;
   a.wim = 0; a.wim_kw = 1; a.wim_ci = a.c_i;
   a.tma_a = 0;
@@ -1101,6 +1154,8 @@ static const Cand kCands[] = {
     // 1x1 layers (TMA-fed A, or staged windows without halo): A rings four chunks deep
     // cover the DRAM latency of the A tiles
     {2, 256, 0, 4, 4, 1, 1}, {2, 128, 0, 4, 6, 1, 1},
+    // probes (tuning cfg only)
+    {1, 128, 0, 2, 6, 1, 2},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
@@ -1164,6 +1219,7 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(47, 1, 256, true, 2, 2, true, 1)
     CGB_SW_CASE(48, 2, 256, false, 4, 4, true, 1)
     CGB_SW_CASE(49, 2, 128, false, 4, 6, true, 1)
+    CGB_SW_CASE(50, 1, 128, false, 2, 6, true, 2)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE

@@ -453,3 +453,35 @@ def test_tf32_truncates_raw_operands(kh, hi, s, p):
     want = _trunc_tf32(F[:, kh // 2, kh // 2, 3])[:, None, None, None] * Ic[None]
     assert O.shape == want.shape
     assert np.array_equal(O, want.astype(np.float32))
+
+
+# ---------------------------------------------------------------- filter-stage groups
+@pytest.mark.parametrize("cp", [
+    dict(k_n=128, k_h=3, k_w=3, c_i=64, h_i=30, w_i=30, b=3, s=2, p=1),   # MT=1 BN=128 pair: 2-tap groups
+    dict(k_n=64, k_h=3, k_w=3, c_i=48, h_i=20, w_i=20, b=2, s=1, p=1),    # BN=64
+    dict(k_n=64, k_h=7, k_w=7, c_i=3, h_i=40, w_i=40, b=2, s=2, p=3),     # w-im2col rows (short taps)
+    dict(k_n=64, k_h=1, k_w=1, c_i=256, h_i=8, w_i=8, b=9, s=1, p=0),     # TMA-fed 1x1: one tap per chunk
+    dict(k_n=128, k_h=1, k_w=1, c_i=192, h_i=7, w_i=7, b=5, s=1, p=0),    # staged 1x1
+])
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_filter_stage_groups_bitwise(orc, cp, prec):
+    """Handing the filter ring over in groups of G taps changes only the synchronisation,
+    never the UMMA order: every group size gives the same bits (and passes the oracle)."""
+    F, I = rand_inputs(cp, 911)
+    dF, dI = to_dev(F), to_dev(I)
+    outs = []
+    for tps in (1, 2, 3, 4, 0):
+        with cg.tuning(tps=tps):
+            outs.append(to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec)))
+    # TMA-fed 1x1 with a single A slot (the forced ring must not deadlock)
+    if cp["k_h"] == 1 and prec == "tf32":
+        for cfg in (20, 22, 26, 29, 31, 32, 33, 34, 35):
+            for tps in (2, 4):
+                with cg.tuning(cfg=cfg, tps=tps):
+                    outs.append(to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec)))
+    ref = orc.conv_gemm(F, I, cp)
+    for o in outs[1:5]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+    for o in outs[5:]:  # other tile configurations: same tolerance, not the same bits
+        assert per_output_error(o, ref, orc.output_scale(F, I, cp)) <= TOL[prec]
+    assert per_output_error(outs[0], ref, orc.output_scale(F, I, cp)) <= TOL[prec]
