@@ -1155,7 +1155,7 @@ static const Cand kCands[] = {
     // cover the DRAM latency of the A tiles
     {2, 256, 0, 4, 4, 1, 1}, {2, 128, 0, 4, 6, 1, 1},
     // probes (tuning cfg only)
-    {1, 128, 0, 2, 6, 1, 2},
+    {1, 128, 0, 2, 6, 1, 2}, {1, 256, 0, 2, 3, 1, 2}, {1, 256, 0, 2, 4, 1, 2},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
@@ -1220,6 +1220,8 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(48, 2, 256, false, 4, 4, true, 1)
     CGB_SW_CASE(49, 2, 128, false, 4, 6, true, 1)
     CGB_SW_CASE(50, 1, 128, false, 2, 6, true, 2)
+    CGB_SW_CASE(51, 1, 256, false, 2, 3, true, 2)
+    CGB_SW_CASE(52, 1, 256, false, 2, 4, true, 2)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE

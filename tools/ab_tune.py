@@ -3,7 +3,8 @@
   python tools/ab_tune.py --layers r50_3x3_s2_56_128,r50_3x3_56_64 --variants '{}' '{"tps":1}' --rounds 7
 
 Each round times every (layer, variant) once, interleaved, as `reps` back-to-back
-launches after an L2 flush (CUDA events); reports the median per (layer, variant) in us.
+launches after an L2 flush (CUDA events); reports the mean per (layer, variant) in us (single-launch event timings are quantised
+to ~2 us on B200, so average many rounds).
 Also `--graph`: the whole 7-layer bench step as one CUDA-graph replay per variant.
 """
 import argparse
@@ -95,5 +96,5 @@ for r in range(a.rounds):
 keys = ["step"] if a.graph else names
 print("variant".ljust(40) + "".join(k[-14:].rjust(15) for k in keys) + "      sum")
 for vi, v in enumerate(variants):
-    meds = [statistics.median(times[(k, vi)]) for k in keys]
+    meds = [statistics.mean(times[(k, vi)]) for k in keys]
     print(json.dumps(v)[:40].ljust(40) + "".join(f"{m:15.1f}" for m in meds) + f"{sum(meds):9.1f}")
