@@ -418,6 +418,9 @@ def run_gpu_arm(args, world, rank, local):
 
     import paper_2005_06410_b200 as cg
     torch.cuda.set_device(local)
+    if args.tune:
+        for k, v in json.loads(args.tune).items():
+            cg.set_tuning(k, v)
     pk = peaks()
     from paper_2005_06410_b200.shard import split_range as shard_split
     b = BATCH  # weak scaling: b=128 per GPU (each rank an independent batch shard)
@@ -530,6 +533,7 @@ def main():
     ap.add_argument("--cpu-batch", type=int, default=2)
     ap.add_argument("--cpu-min-time", type=float, default=2.0)
     ap.add_argument("--ref-batch", type=int, default=2)
+    ap.add_argument("--tune", default="", help='dispatch knobs for A/B runs, JSON, e.g. {"tps": 1}')
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     world, rank, local = dist_setup(args)

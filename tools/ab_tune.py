@@ -46,28 +46,34 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 st = torch.cuda.current_stream()
 
 
-def run_all():
+def run_all(v=None):
+    """The layer list; a variant's knobs apply to every layer, or only to v["only"]."""
+    v = dict(v or {})
+    only = v.pop("only", None)
     for n, cp, F, I, O in tensors:
-        cg.conv(F, I, cp, precision=a.precision, out=O)
+        if only is None or n == only:
+            with cg.tuning(**v):
+                cg.conv(F, I, cp, precision=a.precision, out=O)
+        else:
+            cg.conv(F, I, cp, precision=a.precision, out=O)
 
 
 times = {}
 graphs = {}
 if a.graph:
     for vi, v in enumerate(variants):
-        with cg.tuning(**v):
-            run_all()
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            s2 = torch.cuda.Stream()
-            s2.wait_stream(st)
-            with torch.cuda.stream(s2):
-                run_all()
-            st.wait_stream(s2)
-            torch.cuda.synchronize()
-            with torch.cuda.graph(g):
-                run_all()
-            graphs[vi] = g
+        run_all(v)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s2 = torch.cuda.Stream()
+        s2.wait_stream(st)
+        with torch.cuda.stream(s2):
+            run_all(v)
+        st.wait_stream(s2)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            run_all(v)
+        graphs[vi] = g
 for r in range(a.rounds):
     for vi, v in enumerate(variants):
         if a.graph:
@@ -82,7 +88,9 @@ for r in range(a.rounds):
             torch.cuda.synchronize()
             times.setdefault(("step", vi), []).append(e0.elapsed_time(e1) * 1e3)
             continue
-        with cg.tuning(**v):
+        vv = dict(v)
+        vv.pop("only", None)
+        with cg.tuning(**vv):
             for n, cp, F, I, O in tensors:
                 cg.conv(F, I, cp, precision=a.precision, out=O)  # warm / config
                 flush.zero_()
@@ -94,6 +102,14 @@ for r in range(a.rounds):
                 torch.cuda.synchronize()
                 times.setdefault((n, vi), []).append(e0.elapsed_time(e1) * 1e3 / a.reps)
 keys = ["step"] if a.graph else names
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    print("sm clock now", pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), "MHz; throttle reasons",
+          hex(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+except Exception as e:  # noqa: BLE001
+    print("no nvml", e)
 print("variant".ljust(40) + "".join(k[-14:].rjust(15) for k in keys) + "      sum")
 for vi, v in enumerate(variants):
     meds = [statistics.mean(times[(k, vi)]) for k in keys]
