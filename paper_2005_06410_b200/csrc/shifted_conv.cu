@@ -688,8 +688,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t bt = b_desc0 + (uint64_t)bs * b_stage_units, bt_lo = bt + b_lo_off;
             const uint32_t first = (cc == cc0 && tap == 0) ? 0u : 1u;
             if (!CGB_DBG(2)) {
+              // tail tiles have MT/2 or MT/4 subtiles: unrolled batches for those too
+              constexpr int MT2 = MT >= 2 ? MT / 2 : 1, MT4 = MT >= 4 ? MT / 4 : 1;
               if (full_steps && mtc == MT)
                 issue_tap<MT, BN, SPLIT, PAIR, BK / 8>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first);
+              else if (full_steps && mtc == MT2)
+                issue_tap<MT2, BN, SPLIT, PAIR, BK / 8>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first);
+              else if (full_steps && mtc == MT4)
+                issue_tap<MT4, BN, SPLIT, PAIR, BK / 8>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first);
               else
                 issue_tap_partial<MT, BN, SPLIT, PAIR>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first, mtc,
                                                        a.ksteps);
