@@ -263,6 +263,88 @@ CGB_DEV void issue_tap_partial(uint32_t d_base, uint64_t at, uint64_t at_lo, uin
       }
 }
 
+// Epilogue of one accumulator set: TMEM -> registers -> O for the units u = u0, u0 + du,
+// ... of the tile's (M subtile, 32-column block) pairs, for the 32 rows of TMEM lane
+// quadrant `sub` (the calling warp's warp % 4). add: stream-K piece, red.add into O.
+template <int BN>
+CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, int32_t m0, int n0, int mtc, int sub,
+                         int lane, int u0, int du, bool add) {
+  constexpr int NCB = BN / 32;
+  const int32_t hw_q = a.Hq * a.Wq;
+#pragma unroll 1
+  for (int u = u0; u < mtc * NCB && !CGB_DBG(16); u += du) {
+    const int mt = u / NCB, cb = u - mt * NCB;
+    const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
+    int64_t P = -1;
+    if (Q < a.Mp32) {
+      const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
+      const int32_t rem = Q - bb * hw_q;
+      const int32_t wq = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wq * a.Hq;
+      if (hq < a.h_o && wq < a.w_o) P = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
+    }
+    const uint32_t trow = trow0 + mt * BN;
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(trow + cb * 32, r);
+    tmem_ld_wait();
+    const int nb = n0 + cb * 32;
+    if (a.pstore && a.vec && nb + 32 <= a.k_n && !CGB_DBG(4)) {
+      // Lane pairs write whole 64-byte runs: in store A_k the pair writes segments
+      // 2k, 2k+1 (8 floats each) of the even lane's pixel, in B_k those of the odd
+      // lane's pixel, after one shfl.xor exchange. Each warp store then touches 16
+      // lines with 64 bytes each instead of 32 lines with 32 bytes: half the L1->L2
+      // write requests, which bound the epilogue (~1 request per clock per SM).
+      // (Lane quads writing whole 128-byte lines after a 4x4 shuffle transpose
+      // measured slower: the extra shuffles and selects cost more than they save.)
+      const int par = lane & 1;
+      const int64_t PA = __shfl_sync(0xffffffffu, P, lane & ~1), PB = __shfl_sync(0xffffffffu, P, lane | 1);
+      float* dA = O + PA * a.k_n + nb + 8 * par;
+      float* dB = O + PB * a.k_n + nb + 8 * par;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        uint32_t x[8], v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __shfl_xor_sync(0xffffffffu, par ? r[16 * k + i] : r[16 * k + 8 + i], 1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = par ? x[i] : r[16 * k + i];
+        if (PA >= 0) {
+          if (!add) st_global_v8(dA + 16 * k, v);
+          else {  // stream-K piece: the pair's 16-byte reds share 128-byte lines too
+            red_add_v4(dA + 16 * k, v);
+            red_add_v4(dA + 16 * k + 4, v + 4);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = par ? r[16 * k + 8 + i] : x[i];
+        if (PB >= 0) {
+          if (!add) st_global_v8(dB + 16 * k, v);
+          else {
+            red_add_v4(dB + 16 * k, v);
+            red_add_v4(dB + 16 * k + 4, v + 4);
+          }
+        }
+      }
+    } else if (P >= 0 && !CGB_DBG(4)) {
+      float* dst = O + P * a.k_n + nb;
+      if (a.vec && nb + 32 <= a.k_n) {
+        if (!add) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) st_global_v8(dst + j, &r[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) red_add_v4(dst + j, &r[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (nb + j < a.k_n) {
+            if (!add) dst[j] = __uint_as_float(r[j]);
+            else atomicAdd(dst + j, __uint_as_float(r[j]));
+          }
+      }
+    }
+  }
+}
+
 // PAIR = true: launched as clusters of 2 CTAs (a TPC); the leader (rank 0) issues
 // tcgen05.mma.cta_group::2 with M = 256 -- A rows 0-127 from the leader's window, 128-255
 // from the peer's window at the same shared-memory offset, B split into two halves of
@@ -726,7 +808,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp >= EPI_WARP0) {
     // ---------------------------------------------------------------- epilogue
     const int sub = warp % 4;  // TMEM lane quadrant this warp may access
-    const int32_t hw_q = a.Hq * a.Wq;
     unsigned long long epi_wait = 0, epi_busy = 0;
     int t = 0;
     int tile, cc0, cc1;
@@ -771,80 +852,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           while (ld_acquire_gpu(cnt) < prank) {
           }
       }
-#pragma unroll 1
-      for (int mt = 0; mt < mtc && !CGB_DBG(16); ++mt) {
-        const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
-        int64_t P = -1;
-        if (Q < a.Mp32) {
-          const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
-          const int32_t rem = Q - bb * hw_q;
-          const int32_t wq = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wq * a.Hq;
-          if (hq < a.h_o && wq < a.w_o) P = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
-        }
-        const uint32_t trow = tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS + mt * BN;
-#pragma unroll 1
-        for (int cb = 0; cb < BN / 32; ++cb) {  // 32-column blocks: 32 live data registers
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(trow + cb * 32, r);
-          tmem_ld_wait();
-          const int nb = n0 + cb * 32;
-          if (a.pstore && a.vec && nb + 32 <= a.k_n && !CGB_DBG(4)) {
-            // Lane pairs write whole 64-byte runs: in store A_k the pair writes segments
-            // 2k, 2k+1 (8 floats each) of the even lane's pixel, in B_k those of the odd
-            // lane's pixel, after one shfl.xor exchange. Each warp store then touches 16
-            // lines with 64 bytes each instead of 32 lines with 32 bytes: half the L1->L2
-            // write requests, which bound the epilogue (~1 request per clock per SM).
-            // (Lane quads writing whole 128-byte lines after a 4x4 shuffle transpose
-            // measured slower: the extra shuffles and selects cost more than they save.)
-            const int par = lane & 1;
-            const int64_t PA = __shfl_sync(0xffffffffu, P, lane & ~1), PB = __shfl_sync(0xffffffffu, P, lane | 1);
-            float* dA = O + PA * a.k_n + nb + 8 * par;
-            float* dB = O + PB * a.k_n + nb + 8 * par;
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              uint32_t x[8], v[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) x[i] = __shfl_xor_sync(0xffffffffu, par ? r[16 * k + i] : r[16 * k + 8 + i], 1);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = par ? x[i] : r[16 * k + i];
-              if (PA >= 0) {
-                if (!add) st_global_v8(dA + 16 * k, v);
-                else {  // stream-K piece: the pair's 16-byte reds share 128-byte lines too
-                  red_add_v4(dA + 16 * k, v);
-                  red_add_v4(dA + 16 * k + 4, v + 4);
-                }
-              }
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = par ? r[16 * k + 8 + i] : x[i];
-              if (PB >= 0) {
-                if (!add) st_global_v8(dB + 16 * k, v);
-                else {
-                  red_add_v4(dB + 16 * k, v);
-                  red_add_v4(dB + 16 * k + 4, v + 4);
-                }
-              }
-            }
-          } else if (P >= 0 && !CGB_DBG(4)) {
-            float* dst = O + P * a.k_n + nb;
-            if (a.vec && nb + 32 <= a.k_n) {
-              if (!add) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 8) st_global_v8(dst + j, &r[j]);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) red_add_v4(dst + j, &r[j]);
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (nb + j < a.k_n) {
-                  if (!add) dst[j] = __uint_as_float(r[j]);
-                  else atomicAdd(dst + j, __uint_as_float(r[j]));
-                }
-            }
-          }
-        }
-      }
+      store_units<BN>(a, O, tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS, m0, n0, mtc, sub,
+                      lane, 0, 1, add);
       if (!whole) {
         if (prank + 1 < npieces) {
           __threadfence();  // each lane's rows (stores or reds) before the "written" count
