@@ -88,28 +88,25 @@ def split_range(count, rank, nranks):
 
 
 def peaks():
-    """Roofline denominators. HBM: MEASURED_PEAKS.json. TF32: cuBLAS TF32 measured on this
-    pool the way MEASURED_PEAKS.json measures bf16 (tools/measure_tf32.py ->
-    profiles/tf32_peak.json); bf16/2 when that file is absent."""
-    p = {"hbm_gbs": 6545.6, "bf16_tflops": 1627.7, "src": "MEASURED_PEAKS.json"}
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written on this pool). The
+    TF32 tensor peak is bf16_tflops/2 (dense TF32 runs at half the bf16 rate on tcgen05;
+    the burst figure, since each kernel is timed in a short burst); the HBM peak is
+    hbm_gbs. The cuBLAS TF32 measurement (profiles/tf32_peak.json) is context only --
+    our kernels exceed it, so it is not a peak."""
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             m = json.load(f)
-        p["hbm_gbs"] = float(m["hbm_gbs"])
-        p["bf16_tflops"] = float(m["bf16_tflops"])
-    except Exception:
-        p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
-    p["tf32_from_bf16"] = p["bf16_tflops"] / 2.0  # dense TF32 = 1/2 dense BF16 on tcgen05
-    p["tf32_tflops"] = p["tf32_from_bf16"]
-    p["tf32_src"] = f"bf16_tflops/2 from {p['src']} (of measured)"
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "bf16_tflops": float(m["bf16_tflops"]), "src": "MEASURED_PEAKS.json"}
+    except Exception:  # noqa: BLE001
+        pass
+    p["tf32_tflops"] = p["bf16_tflops"] / 2.0
+    p["tf32_src"] = f"bf16_tflops/2 of {p['src']} (burst; dense TF32 = half the dense bf16 rate on tcgen05)"
     try:
         with open(os.path.join(ROOT, "profiles", "tf32_peak.json")) as f:
-            t = json.load(f)
-        p["tf32_tflops"] = float(t["tf32_tflops"])
-        p["tf32_src"] = ("measured: cuBLAS TF32 8192^3 burst on this pool (profiles/tf32_peak.json, "
-                         "tools/measure_tf32.py; same method as MEASURED_PEAKS.json's bf16)")
-    except Exception:
-        pass
+            p["cublas_tf32"] = float(json.load(f)["tf32_tflops"])
+    except Exception:  # noqa: BLE001
+        p["cublas_tf32"] = None
     return p
 
 
@@ -229,58 +226,60 @@ def max_over_ranks(x, world):
 
 
 # ----------------------------------------------------------------------------- CPU reference
-def cpu_reference_time(batch_sample, min_time, threads, rng_seed=20177):
-    """The reference's own conv_gemm<float> (oracle/_ref, compiled from /root/reference)
-    timed with its repeat-until-min_time loop (proj/src/bench.cpp:200-210)."""
-    import numpy as np
-    from oracle.oracle import REFERENCE_SO, Reference, Restatement
-    kind = "reference"
+def _ref_runner(threads):
+    """The reference's own conv_gemm<float> (oracle/_ref, compiled from /root/reference);
+    the plain-C port (oracle/) only where the reference build is absent."""
+    from oracle.oracle import Reference, Restatement
     try:
         ref = Reference()
-        run = lambda F, I, cp: ref.conv_gemm(F, I, cp, threads=threads)  # noqa: E731
-    except Exception:
-        kind = "port"
+        return (lambda F, I, cp: ref.conv_gemm(F, I, cp, threads=threads)), "reference"
+    except Exception:  # noqa: BLE001
         orc = Restatement()
-        run = lambda F, I, cp: orc.conv_gemm(F, I, cp)  # noqa: E731
-    rng = np.random.default_rng(rng_seed)
-    total_flops, total_t = 0, 0.0
-    for layer in LAYERS:
-        cp = layer_cp(layer, batch_sample)
+        return (lambda F, I, cp: orc.conv_gemm(F, I, cp)), "port"
+
+
+def host_tensors(layers, b, seed=20177):
+    """Seeded host tensors (Fortran order, the reference layouts) for the CPU arms."""
+    import numpy as np
+    out = []
+    for layer in layers:
+        cp = layer_cp(layer, b)
+        rng = np.random.default_rng(layer_seed(layer[0], seed))
         F = np.asfortranarray(rng.uniform(-1, 1, (cp["k_n"], 3, 3, cp["c_i"])).astype(np.float32))
         I = np.asfortranarray(rng.uniform(-1, 1, (cp["h_i"], cp["w_i"], cp["c_i"], cp["b"])).astype(np.float32))
-        reps, t0 = 0, time.perf_counter()
-        while True:
-            run(F, I, cp)
-            reps += 1
-            el = time.perf_counter() - t0
-            if el >= min_time:
-                break
-        total_flops += flops(cp) * reps
-        total_t += el
-    return total_flops / total_t / 1e9, kind, total_t
+        out.append((layer, cp, F, I))
+    return out
 
 
 def run_reference_arm(args, world, rank):
+    """The reference arm: the reference's CPU conv_gemm on the box's host cores, same
+    metric/config as the GPU arm. Each step is the 7 layers at the full b=128 (the real
+    config; ~4 s per step at ~50 GFLOPS on 16 cores) unless --ref-batch asks for a sample."""
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    sample_b = args.ref_batch
-    # warm-up steps
-    for _ in range(args.warmup):
-        cpu_reference_time(sample_b, 0.0, threads)
-    vals = []
-    t_all = 0.0
+    run, kind = _ref_runner(threads)
+    sample_b = args.ref_batch or BATCH
+    data = host_tensors(LAYERS, sample_b)
+    warm = host_tensors(LAYERS, 1)
+    for _ in range(args.warmup):  # warm-up steps on one image (page-in, thread team)
+        for layer, cp, F, I in warm:
+            run(F, I, cp)
+    step_t = []
     for _ in range(args.steps):
-        v, kind, t = cpu_reference_time(sample_b, 0.0, threads)
-        vals.append(v)
-        t_all += t
-    value = statistics.mean(vals)
-    step_flops = sum(flops(layer_cp(l, sample_b)) for l in LAYERS)
+        t0 = time.perf_counter()
+        for layer, cp, F, I in data:
+            run(F, I, cp)
+        step_t.append(time.perf_counter() - t0)
+    step_flops = sum(flops(cp) for _, cp, _, _ in data)
+    value = step_flops / statistics.mean(step_t) / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / max(args.steps, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "ResNet-50 v1.5 3x3 convs (BASELINE configs[1])", "global_batch": BATCH,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(step_t),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (uniform[-1,1], seeded numpy)",
+        "config": {"workload": "ResNet-50 v1.5 3x3 convs at b=128 (BASELINE configs[1])", "global_batch": BATCH,
+                   "batch_per_step": sample_b, "same_config": sample_b == BATCH,
                    "layers": [l[0] for l in LAYERS], "algo": "conv_gemm (reference fused ConvGemm)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"each step = the 7 layers at b={sample_b} (of {BATCH}), "
@@ -291,10 +290,42 @@ def run_reference_arm(args, world, rank):
     return 0
 
 
+def host_image_batch(t, b0, b1):
+    """Images [b0, b1) of a leftmost-fastest CUDA tensor as a Fortran numpy array."""
+    import numpy as np
+    x = t[..., b0:b1]
+    flat = x.permute(3, 2, 1, 0).contiguous().view(-1).cpu().numpy()
+    return np.asfortranarray(flat.reshape(tuple(x.shape), order="F"))
+
+
+def cpu_baseline_leg(tensors, nimg, min_time, threads):
+    """cpu_baseline: the reference's conv_gemm on the first `nimg` images of the SAME
+    inputs the GPU ran, repeat-until-min_time per layer (bench.cpp:200-210); its outputs
+    double as a parity check of the GPU outputs of those images (returned per layer)."""
+    from oracle.oracle import Restatement, per_output_error
+    run, kind = _ref_runner(threads)
+    orc = Restatement()
+    total_flops, total_t, parity = 0, 0.0, {}
+    for layer, cp, F, I, O in tensors:
+        cpn = dict(cp, b=nimg)
+        Fh = host_image_batch(F, 0, F.shape[3])
+        Ih, Oh = host_image_batch(I, 0, nimg), host_image_batch(O, 0, nimg)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            ref = run(Fh, Ih, cpn)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= min_time:
+                break
+        total_flops += flops(cpn) * reps
+        total_t += el
+        parity[layer[0]] = per_output_error(Oh, ref, orc.output_scale(Fh, Ih, cpn))
+    return total_flops / total_t / 1e9, kind, total_t, parity
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def make_layer_tensors(cg, torch, layers, b, rank, world, seed=20177):
     out = []
-    g = torch.Generator(device="cuda").manual_seed(seed + 1000 * rank)
     for layer in layers:
         cp = layer_cp(layer, b)
         h_o, w_o = out_hw(cp)
@@ -304,8 +335,9 @@ def make_layer_tensors(cg, torch, layers, b, rank, world, seed=20177):
         if world > 1:
             from paper_2005_06410_b200.shard import broadcast_filters
             broadcast_filters(F, src=0)  # filters broadcast once, outside the timed region
+        gi = torch.Generator(device="cuda").manual_seed(layer_seed(layer[0], seed + 1 + rank))
         I = cg.empty_tensor4(cp["h_i"], cp["w_i"], cp["c_i"], b)
-        I.copy_(torch.rand(I.shape, generator=g, device="cuda") * 2 - 1)
+        I.copy_(torch.rand(I.shape, generator=gi, device="cuda") * 2 - 1)
         O = cg.empty_tensor4(cp["k_n"], h_o, w_o, b)
         out.append((layer, cp, F, I, O))
     return out
@@ -316,6 +348,7 @@ L2_NOTE = {
     "cycle": "no flush: inputs larger than L2 - the 7 layers' inputs (577 MB, 4.6x the 126 MB L2) are "
              "read in turn, so every layer's input was evicted by the other six since its last use",
 }
+TOL = {"tf32": 5e-3, "3xtf32": 1e-5, "auto": 1e-5}
 
 
 def time_mode(cg, torch, tensors, precision, steps, warmup, flush, world, clocks=None):
@@ -378,6 +411,7 @@ def time_mode(cg, torch, tensors, precision, steps, warmup, flush, world, clocks
     del g
     return per_layer, step_ms, launches_per_step * steps, clk
 
+
 def time_e2e(cg, torch, tensors, precision, steps, warmup, world):
     """Public host-buffer API (cgb_conv_host via cg.conv on numpy arrays backed by
     pinned memory): H2D of F and I, the kernel, D2H of O, every step."""
@@ -413,6 +447,14 @@ def time_e2e(cg, torch, tensors, precision, steps, warmup, world):
     return e0.elapsed_time(e1) / steps, h2d, d2h
 
 
+def parity_fp64(torch, tensors):
+    """Per layer: max north-star per-output error of the outputs just timed against an
+    fp64 recomputation of EVERY output (tests/fp64ref.py; after the timed region)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from fp64ref import per_output_error_fp64
+    return {layer[0]: per_output_error_fp64(torch, F, I, O, cp) for layer, cp, F, I, O in tensors}
+
+
 def run_gpu_arm(args, world, rank, local):
     import torch
 
@@ -430,8 +472,12 @@ def run_gpu_arm(args, world, rank, local):
     tensors = make_layer_tensors(cg, torch, LAYERS, b, rank, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.l2 == "flush" else None
     clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    step_flops_local = sum(flops(cp) for _, cp, _, _, _ in tensors)
+    total_flops = step_flops_local * world if args.scaling == "weak" else sum(flops(layer_cp(l, BATCH)) for l in LAYERS)
 
     modes = {}
+    parity = {}
+    cpu = None
     headline = args.precision
     order = [headline] + [m for m in ("3xtf32",) if m != headline and not args.quick]
     for prec in order:
@@ -439,11 +485,7 @@ def run_gpu_arm(args, world, rank, local):
                                                     clocks if prec == headline else None)
         if prec == headline:
             clk = c
-        ms_step = statistics.mean(step_ms)
-        ms_step = max_over_ranks(ms_step, world)
-        step_flops_local = sum(flops(cp) for _, cp, _, _, _ in tensors)
-        total_flops = step_flops_local * world if args.scaling == "weak" else \
-            sum(flops(layer_cp(l, BATCH)) for l in LAYERS)
+        ms_step = max_over_ranks(statistics.mean(step_ms), world)
         layers = []
         for li, (layer, cp, F, I, O) in enumerate(tensors):
             t = statistics.mean(per_layer[li]) * 1e-3
@@ -453,34 +495,49 @@ def run_gpu_arm(args, world, rank, local):
             layers.append({"layer": layer[0], "ms": round(t * 1e3, 4), "gflops": round(fl / t / 1e9, 1),
                            "tflops": round(fl / t / 1e12, 1), "hbm_gbs": round(by / t / 1e9, 1),
                            "bound": "tensor" if t_tc >= t_hbm else "hbm",
-                           "roofline_frac": round(max(t_tc, t_hbm) / t, 4),
-                           "tf32_frac": round(t_tc / t, 4)})
+                           "roofline_frac": round(max(t_tc, t_hbm) / t, 4)})
         modes[prec] = {"value": total_flops / (ms_step * 1e-3) / 1e9, "ms_per_step": ms_step,
                        "layers": layers, "gpu_launches": launches,
                        "achieved_tflops": step_flops_local / (ms_step * 1e-3) / 1e12}
-    # e2e through the host-buffer public API (headline precision)
-    e2e_ms, h2d, d2h = time_e2e(cg, torch, tensors, headline, max(1, min(args.steps, 3)), 1, world)
-    e2e_ms = max_over_ranks(e2e_ms, world)
+        # parity of the outputs just timed (outside the timed region)
+        if not args.no_parity:
+            errs = parity_fp64(torch, tensors)
+            parity[prec] = {"check": "fp64 recomputation of every output of every layer (cuDNN fp64 on the "
+                                     "device, tests/fp64ref.py), per-output error normalised by "
+                                     "||F[i_k]||*||B[:,col]||",
+                            "tolerance": TOL[prec], "max_err": {k: float(f"{v:.3e}") for k, v in errs.items()},
+                            "pass": all(v <= TOL[prec] for v in errs.values())}
+        if prec == headline and world == 1 and rank == 0 and not args.no_cpu_baseline:
+            v, kind, t, ref_err = cpu_baseline_leg(tensors, args.cpu_batch, args.cpu_min_time, os.cpu_count() or 1)
+            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind,
+                   "sample": f"the 7 layers on images 0..{args.cpu_batch - 1} of the GPU inputs (b={args.cpu_batch} of "
+                             f"{BATCH}), conv_gemm<float> repeated until >= {args.cpu_min_time}s per layer "
+                             f"({t:.1f}s CPU total), threads=nproc"}
+            parity["reference_sample"] = {
+                "check": f"the reference's own conv_gemm output (cpu_baseline leg) vs the GPU {headline} output, "
+                         f"images 0..{args.cpu_batch - 1} of the full-batch launch",
+                "tolerance": TOL[headline], "max_err": {k: float(f"{e:.3e}") for k, e in ref_err.items()},
+                "pass": all(e <= TOL[headline] for e in ref_err.values())}
+    # e2e through the host-buffer public API, every measured precision
+    e2e = {}
+    for prec in order:
+        e2e_ms, h2d, d2h = time_e2e(cg, torch, tensors, prec, max(1, min(args.steps, 3)), 1, world)
+        e2e_ms = max_over_ranks(e2e_ms, world)
+        e2e[prec] = {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                     "api": "cgb_conv_host (host buffers, pinned)"}
     if rank != 0:
         return 0
     hm = modes[headline]
-    step_flops_local = sum(flops(cp) for _, cp, _, _, _ in tensors)
-    total_flops = step_flops_local * world if args.scaling == "weak" else \
-        sum(flops(layer_cp(l, BATCH)) for l in LAYERS)
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        v, kind, t = cpu_reference_time(args.cpu_batch, args.cpu_min_time, os.cpu_count() or 1)
-        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind,
-               "sample": f"the 7 layers at b={args.cpu_batch} (of {BATCH}), conv_gemm<float> repeated until "
-                         f">= {args.cpu_min_time}s per layer ({t:.1f}s CPU total), threads=nproc"}
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
                 traffic = json.load(f).get(headline)
-        except Exception:
+        except Exception:  # noqa: BLE001
             traffic = None
+    peak = pk["tf32_tflops"]
     line = {
         "metric": METRIC, "value": hm["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": hm["ms_per_step"], "higher_is_better": True,
@@ -492,25 +549,27 @@ def run_gpu_arm(args, world, rank, local):
                    "l2": L2_NOTE[args.l2],
                    "launch": "one CUDA-graph replay of the 7 layer launches per step (programmatic dependent launch "
                              "between kernels); per-layer times from an eager pass",
-                   "parallelism": f"batch-sharded dp{world}, no collective in the timed region"},
-        "roofline": {"bound": "tensor", "achieved": hm["achieved_tflops"], "peak": pk["tf32_tflops"],
-                     "unit": "TFLOP/s", "frac": hm["achieved_tflops"] / pk["tf32_tflops"], "traffic": traffic,
+                   "parallelism": f"batch-sharded dp{world} ({args.scaling} scaling), no collective in the timed "
+                                  f"region"},
+        "roofline": {"bound": "tensor", "achieved": hm["achieved_tflops"], "peak": peak,
+                     "unit": "TFLOP/s", "frac": hm["achieved_tflops"] / peak, "traffic": traffic,
                      "peak_src": pk["tf32_src"],
                      "frac_vs_other_peaks": {
-                         "bf16_tflops/2 of MEASURED_PEAKS.json": hm["achieved_tflops"] / pk["tf32_from_bf16"],
-                         "nominal dense TF32 1100 (B200_PROFILING.md table)": hm["achieved_tflops"] / 1100.0,
-                         "tcgen05 UMMA microbenchmark 1151 @1.9 GHz (tools/umma_bench.cu)":
-                             hm["achieved_tflops"] / 1151.0},
+                         "cuBLAS TF32 8192^3 burst on this pool (profiles/tf32_peak.json)":
+                             hm["achieved_tflops"] / pk["cublas_tf32"] if pk.get("cublas_tf32") else None,
+                         "tcgen05 kind::tf32 UMMA microbenchmark 1190 @1965 MHz (tools/umma_bench.cu, pair_bench.cu)":
+                             hm["achieved_tflops"] / 1190.0},
                      "per_layer": hm["layers"]},
+        "parity": parity,
         "cpu_baseline": cpu,
-        "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": "cgb_conv_host (host buffers, pinned)"},
+        "e2e": e2e[headline],
         "gpu_launches": hm["gpu_launches"],
         "clocks": clk,
         "modes": {m: {"value": v["value"], "ms_per_step": v["ms_per_step"],
-                      "tf32_frac": v["achieved_tflops"] / pk["tf32_tflops"],
+                      "tf32_frac": v["achieved_tflops"] / peak,
                       # 3xTF32 issues three TF32 MMAs per product: its own roofline is P_TF32/3
-                      "frac_of_own_roofline": v["achieved_tflops"] / (pk["tf32_tflops"] / (3 if m == "3xtf32" else 1)),
+                      "frac_of_own_roofline": v["achieved_tflops"] / (peak / (3 if m == "3xtf32" else 1)),
+                      "e2e": e2e[m],
                       "per_layer_tflops": {l["layer"]: l["tflops"] for l in v["layers"]}} for m, v in modes.items()},
     }
     print(json.dumps(line), flush=True)
@@ -524,7 +583,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="tf32", choices=["tf32", "3xtf32", "auto"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): the global b=128 split across ranks (threads.hpp:20-25); "
+                         "weak: b=128 per rank")
     ap.add_argument("--quick", action="store_true", help="headline precision only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--l2", choices=sorted(L2_NOTE), default="flush",
@@ -532,7 +593,8 @@ def main():
                          "inputs (577 MB) are larger than L2")
     ap.add_argument("--cpu-batch", type=int, default=2)
     ap.add_argument("--cpu-min-time", type=float, default=2.0)
-    ap.add_argument("--ref-batch", type=int, default=2)
+    ap.add_argument("--ref-batch", type=int, default=0, help="reference arm batch per step (0 = the full b=128)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the fp64 parity pass after timing")
     ap.add_argument("--tune", default="", help='dispatch knobs for A/B runs, JSON, e.g. {"tps": 1}')
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
