@@ -117,13 +117,20 @@ cgb_status cgb_conv_host(int algo, int precision, const float* F_host, const flo
                          const cgb_conv_params* cp, float* O_host, void* stream);
 
 /* ---- workspace accounting (ScratchTracker equivalent, scratch.hpp:14-28) ----
- * Counts device workspace the library allocates itself. A non-zero limit turns
- * oversized requests into CGB_ALLOCATION_FAILURE (scratch.cpp:15-19). */
+ * Every call that needs device workspace (and was given none) claims its size: the
+ * claim is checked against the limit on every call (non-zero limit -> oversized claims
+ * fail with CGB_ALLOCATION_FAILURE, scratch.cpp:15-19) and counted in current/peak
+ * while the call runs on the host (current returns to 0 between calls). The library
+ * caches one buffer per (device, stream); buffers used while a stream was being
+ * captured into a CUDA graph are never freed implicitly. */
 uint64_t cgb_scratch_current_bytes(void);
 uint64_t cgb_scratch_peak_bytes(void);
 void cgb_scratch_reset_peak(void);
 void cgb_scratch_set_limit(uint64_t bytes);
-void cgb_scratch_release(void); /* free the cached workspace */
+/* Free every cached workspace buffer (graphs captured earlier must not be replayed). */
+void cgb_scratch_release(void);
+/* Bytes currently held by the per-(device, stream) workspace caches. */
+uint64_t cgb_scratch_cached_bytes(void);
 
 /* ---- dispatch policy (no reference equivalent: the reference's BlockingParams are
  * CPU cache blocking, validated and otherwise ignored here) ----

@@ -20,6 +20,7 @@ SYMBOLS = (
     "cgb_gemm", "cgb_conv_host", "cgb_scratch_current_bytes", "cgb_scratch_peak_bytes", "cgb_scratch_reset_peak",
     "cgb_scratch_set_limit", "cgb_scratch_release", "cgb_last_error", "cgb_version",
     "cgb_kernel_launch_count", "cgb_last_path", "cgb_debug_sw_stats", "cgb_set_tuning", "cgb_get_tuning",
+    "cgb_scratch_cached_bytes",
 )
 
 
@@ -59,6 +60,7 @@ def _load() -> ctypes.CDLL:
         "cgb_scratch_reset_peak": (None, []),
         "cgb_scratch_set_limit": (None, [ctypes.c_uint64]),
         "cgb_scratch_release": (None, []),
+        "cgb_scratch_cached_bytes": (ctypes.c_uint64, []),
         "cgb_last_error": (ctypes.c_char_p, []),
         "cgb_version": (ctypes.c_char_p, []),
         "cgb_kernel_launch_count": (ctypes.c_uint64, []),

@@ -14,7 +14,9 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <vector>
 #include <string>
 #include <type_traits>
 
@@ -173,52 +175,75 @@ cudaError_t make_input_tmap_1x1(CUtensorMap* tm, const float* i, const ConvGeom&
 }
 
 // ------------------------------------------------------------------ workspace (ScratchTracker)
-struct Scratch {
-  std::mutex mu;
+// One cached device buffer per (device, stream): calls on different streams (which may
+// run concurrently) never share workspace, like the stream-K counters. Accounting
+// follows the reference's ScratchTracker (scratch.cpp:12-52): every call claims `need`
+// bytes -- checked against the limit on EVERY call, cached buffer or not -- and
+// current/peak count the claimed bytes of in-flight claims (released when the call has
+// been enqueued), independent of the size of the cached allocation. A buffer that was
+// in use while its stream was being captured into a CUDA graph may be referenced by
+// that graph: it is never freed implicitly (retired to a list that only
+// cgb_scratch_release frees; replaying graphs captured before a release is the
+// caller's error, as freeing any buffer a graph uses).
+struct WsBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
-  int device = -1;
+  bool captured = false;  // used during a stream capture at least once
+};
+struct Scratch {
+  std::mutex mu;
+  std::map<std::pair<int, cudaStream_t>, WsBuf> bufs;
+  std::vector<void*> retired;  // captured buffers that were outgrown
   std::atomic<uint64_t> current{0}, peak{0}, limit{0};
 };
 static Scratch g_scratch;
 
-static cgb_status scratch_get(size_t need, void** out, cudaStream_t st) {
-  std::lock_guard<std::mutex> lk(g_scratch.mu);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (g_scratch.ptr && g_scratch.bytes >= need && g_scratch.device == dev) {
-    *out = g_scratch.ptr;
-    return CGB_OK;
+static void scratch_account(uint64_t need) {
+  const uint64_t cur = g_scratch.current.fetch_add(need) + need;
+  uint64_t seen = g_scratch.peak.load();
+  while (seen < cur && !g_scratch.peak.compare_exchange_weak(seen, cur)) {
   }
+}
+
+// Claim `need` bytes of workspace for one call on stream st; the claim is released
+// with scratch_done(need) once the call's kernels are enqueued.
+static cgb_status scratch_get(size_t need, void** out, cudaStream_t st) {
   const uint64_t lim = g_scratch.limit.load();
-  const uint64_t keep = (g_scratch.device == dev) ? 0 : 0;
-  (void)keep;
   if (lim != 0 && need > lim)
     return fail(CGB_ALLOCATION_FAILURE, "workspace limit exceeded: " + std::to_string(need) +
                                             " bytes requested, limit " + std::to_string(lim));
-  if (g_scratch.ptr) {
-    // cudaFree synchronises (no kernel still reads the old buffer); while a graph is
-    // being captured the old buffer is leaked instead (freeing would break the capture)
-    if (can_free_now(st)) cudaFree(g_scratch.ptr);
-    g_scratch.current.store(0);
-    g_scratch.ptr = nullptr;
-    g_scratch.bytes = 0;
+  std::lock_guard<std::mutex> lk(g_scratch.mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  WsBuf& w = g_scratch.bufs[{dev, st}];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    cs = cudaStreamCaptureStatusActive;  // unknown: treat as captured (never free)
   }
-  void* p = nullptr;
-  const size_t alloc = std::max<size_t>(need, size_t(1) << 20);
-  if (capture_safe_malloc(&p, alloc) != cudaSuccess) {
-    return fail(CGB_ALLOCATION_FAILURE, "cannot allocate " + std::to_string(alloc) + " bytes of device workspace");
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  if (!w.ptr || w.bytes < need) {
+    if (w.ptr) {
+      // cudaFree synchronises the device, so no kernel still reads it -- unless a
+      // captured graph refers to it: retire instead of freeing
+      if (w.captured || capturing) g_scratch.retired.push_back(w.ptr);
+      else cudaFree(w.ptr);
+      w = WsBuf{};
+    }
+    void* p = nullptr;
+    const size_t alloc = std::max<size_t>(need, size_t(1) << 20);
+    if (capture_safe_malloc(&p, alloc) != cudaSuccess)
+      return fail(CGB_ALLOCATION_FAILURE, "cannot allocate " + std::to_string(alloc) + " bytes of device workspace");
+    w.ptr = p;
+    w.bytes = alloc;
   }
-  g_scratch.ptr = p;
-  g_scratch.bytes = alloc;
-  g_scratch.device = dev;
-  g_scratch.current.store(alloc);
-  uint64_t seen = g_scratch.peak.load();
-  while (seen < alloc && !g_scratch.peak.compare_exchange_weak(seen, alloc)) {
-  }
-  *out = p;
+  w.captured = w.captured || capturing;
+  scratch_account(need);
+  *out = w.ptr;
   return CGB_OK;
 }
+
+static void scratch_done(size_t need) { g_scratch.current.fetch_sub(need); }
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -327,6 +352,7 @@ static cgb_status conv_impl(int algo, int precision, const float* F, const float
   const bool wim = !Bext && use_wim(algo, prec, g);
   const size_t need = std::max<size_t>((size_t)(pl.f_bytes + pl.b_bytes), wim ? (size_t)wim_filter_bytes(prec, g) : 0);
   uint8_t* ws = nullptr;
+  size_t claimed = 0;
   if (need > 0) {
     if (workspace) {
       if (workspace_bytes < need)
@@ -336,8 +362,15 @@ static cgb_status conv_impl(int algo, int precision, const float* F, const float
       void* p = nullptr;
       if ((st = scratch_get(need, &p, s))) return st;
       ws = static_cast<uint8_t*>(p);
+      claimed = need;
     }
   }
+  struct Release {
+    size_t n;
+    ~Release() {
+      if (n) scratch_done(n);
+    }
+  } release{claimed};
   cudaError_t e;
   // Filters for the tensor-core paths.
   const float* f_hi = F;
@@ -539,11 +572,26 @@ uint64_t cgb_scratch_peak_bytes(void) { return g_scratch.peak.load(); }
 void cgb_scratch_reset_peak(void) { g_scratch.peak.store(g_scratch.current.load()); }
 void cgb_scratch_set_limit(uint64_t bytes) { g_scratch.limit.store(bytes); }
 void cgb_scratch_release(void) {
+  // frees every cached workspace, captured or not: graphs captured before this call must
+  // not be replayed afterwards
   std::lock_guard<std::mutex> lk(g_scratch.mu);
-  if (g_scratch.ptr) cudaFree(g_scratch.ptr);
-  g_scratch.ptr = nullptr;
-  g_scratch.bytes = 0;
-  g_scratch.current.store(0);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : g_scratch.bufs)
+    if (kv.second.ptr) {
+      cudaSetDevice(kv.first.first);
+      cudaFree(kv.second.ptr);
+    }
+  for (void* p : g_scratch.retired) cudaFree(p);
+  cudaSetDevice(cur);
+  g_scratch.bufs.clear();
+  g_scratch.retired.clear();
+}
+uint64_t cgb_scratch_cached_bytes(void) {
+  std::lock_guard<std::mutex> lk(g_scratch.mu);
+  uint64_t n = 0;
+  for (auto& kv : g_scratch.bufs) n += kv.second.bytes;
+  return n;
 }
 
 cgb_status cgb_set_tuning(const char* key, int64_t value) {

@@ -33,9 +33,14 @@ namespace cgb {
 namespace {
 
 // Persistent memcpy pool. A job is up to two (dst, src, n) segments cut into
-// 1 MiB-aligned pieces that the caller and the workers claim with an atomic counter.
-// Workers spin on the job generation for a while before sleeping, so the per-job
-// hand-off costs about a cache-line transfer rather than a futex wake-up.
+// 1 MiB-aligned pieces that the caller and the workers claim with one 64-bit atomic
+// holding (job generation << 32 | next piece), so a claim can only succeed for the job
+// it was read for. Job descriptors are double-buffered by generation parity, and a
+// descriptor is rewritten only when no thread is inside the job two generations back
+// (active_ counts per slot, re-checked against the generation after entering): a late
+// worker can never copy or count a piece of a job it did not claim from. Workers spin
+// on the generation for a while before sleeping, so the per-job hand-off costs about a
+// cache-line transfer rather than a futex wake-up.
 class CopyPool {
  public:
   struct Seg {
@@ -47,7 +52,7 @@ class CopyPool {
     static CopyPool pool;
     return pool;
   }
-  // both segments copied when this returns
+  // both segments copied when this returns (callers are serialised)
   void copy2(Seg a, Seg b) {
     const size_t total = a.n + b.n;
     if (total == 0) return;
@@ -56,25 +61,33 @@ class CopyPool {
       if (b.n) std::memcpy(b.dst, b.src, b.n);
       return;
     }
-    seg_[0] = a;
-    seg_[1] = b;
+    std::lock_guard<std::mutex> caller(caller_mu_);
+    const uint64_t g = ++gen_;  // caller-owned counter
+    const int slot = (int)(g & 1);
+    while (active_[slot].load(std::memory_order_acquire) != 0) cpu_relax();  // stragglers of job g - 2
+    Job& j = jobs_[slot];
+    j.seg[0] = a;
+    j.seg[1] = b;
     const size_t parts = std::min<size_t>(4 * (workers_.size() + 1), (total + kPiece - 1) / kPiece);
-    per_ = (total + parts - 1) / parts;
-    per_ = (per_ + 4095) & ~size_t(4095);
-    nparts_ = (int)((total + per_ - 1) / per_);
-    pending_.store(nparts_, std::memory_order_relaxed);
-    next_.store(0, std::memory_order_release);  // a straggler claiming from here sees this job
-    gen_.fetch_add(1, std::memory_order_release);  // publishes the job
+    j.per = ((total + parts - 1) / parts + 4095) & ~size_t(4095);
+    j.nparts = (uint32_t)((total + j.per - 1) / j.per);
+    pending_.store((int)j.nparts, std::memory_order_relaxed);
+    claim_.store(g << 32, std::memory_order_release);  // publishes the job
     if (sleepers_.load(std::memory_order_acquire) > 0) {
       std::lock_guard<std::mutex> lk(mu_);
       cv_.notify_all();
     }
-    work();
+    work(g);
     while (pending_.load(std::memory_order_acquire) > 0) cpu_relax();
   }
 
  private:
   static constexpr size_t kPiece = size_t(1) << 20;
+  struct Job {
+    Seg seg[2] = {};
+    size_t per = 0;
+    uint32_t nparts = 0;
+  };
   static void cpu_relax() {
 #if defined(__x86_64__)
     __builtin_ia32_pause();
@@ -94,50 +107,57 @@ class CopyPool {
     }
     for (auto& t : workers_) t.join();
   }
-  // claim and copy pieces of the current job until none are left
-  void work() {
-    for (;;) {
-      const int i = next_.fetch_add(1, std::memory_order_acq_rel);
-      if (i >= nparts_) return;
-      size_t lo = (size_t)i * per_, hi = std::min(lo + per_, seg_[0].n + seg_[1].n);
-      for (int k = 0; k < 2 && lo < hi; ++k) {  // the piece may straddle the two segments
-        const Seg& sg = seg_[k];
-        if (lo < sg.n) {
-          const size_t e = std::min(hi, sg.n);
-          std::memcpy(static_cast<char*>(sg.dst) + lo, static_cast<const char*>(sg.src) + lo, e - lo);
+  // claim and copy pieces of job g until none are left (or a newer job replaced it)
+  void work(uint64_t g) {
+    const int slot = (int)(g & 1);
+    active_[slot].fetch_add(1, std::memory_order_acq_rel);
+    if ((claim_.load(std::memory_order_acquire) >> 32) == g) {
+      const Job& j = jobs_[slot];
+      for (;;) {
+        uint64_t c = claim_.load(std::memory_order_acquire);
+        if ((c >> 32) != g || (uint32_t)c >= j.nparts) break;
+        if (!claim_.compare_exchange_weak(c, c + 1, std::memory_order_acq_rel)) continue;
+        size_t lo = (size_t)(uint32_t)c * j.per, hi = std::min(lo + j.per, j.seg[0].n + j.seg[1].n);
+        for (int k = 0; k < 2 && lo < hi; ++k) {  // the piece may straddle the two segments
+          const Seg& sg = j.seg[k];
+          if (lo < sg.n) {
+            const size_t e = std::min(hi, sg.n);
+            std::memcpy(static_cast<char*>(sg.dst) + lo, static_cast<const char*>(sg.src) + lo, e - lo);
+          }
+          lo = lo > sg.n ? lo - sg.n : 0;
+          hi = hi > sg.n ? hi - sg.n : 0;
         }
-        lo = lo > sg.n ? lo - sg.n : 0;
-        hi = hi > sg.n ? hi - sg.n : 0;
+        pending_.fetch_sub(1, std::memory_order_acq_rel);
       }
-      pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
+    active_[slot].fetch_sub(1, std::memory_order_release);
   }
   void run() {
-    uint64_t seen = gen_.load(std::memory_order_acquire);
+    uint64_t seen = claim_.load(std::memory_order_acquire) >> 32;
     for (;;) {
       // spin ~100 us for the next job, then sleep
-      for (int it = 0; it < 20000 && gen_.load(std::memory_order_acquire) == seen && !stop_.load(); ++it)
+      for (int it = 0; it < 20000 && (claim_.load(std::memory_order_acquire) >> 32) == seen && !stop_.load(); ++it)
         cpu_relax();
-      if (gen_.load(std::memory_order_acquire) == seen) {
+      if ((claim_.load(std::memory_order_acquire) >> 32) == seen) {
         std::unique_lock<std::mutex> lk(mu_);
         sleepers_.fetch_add(1, std::memory_order_acq_rel);
-        cv_.wait(lk, [&] { return stop_.load() || gen_.load(std::memory_order_acquire) != seen; });
+        cv_.wait(lk, [&] { return stop_.load() || (claim_.load(std::memory_order_acquire) >> 32) != seen; });
         sleepers_.fetch_sub(1, std::memory_order_acq_rel);
       }
       if (stop_.load()) return;
-      seen = gen_.load(std::memory_order_acquire);
-      work();
+      seen = claim_.load(std::memory_order_acquire) >> 32;
+      work(seen);
     }
   }
 
   std::vector<std::thread> workers_;
-  std::mutex mu_;
+  std::mutex mu_, caller_mu_;
   std::condition_variable cv_;
-  Seg seg_[2] = {};
-  size_t per_ = 0;
-  int nparts_ = 0;
-  std::atomic<int> next_{0}, pending_{0}, sleepers_{0};
-  std::atomic<uint64_t> gen_{0};
+  Job jobs_[2];
+  uint64_t gen_ = 0;                    // last published job (caller only)
+  std::atomic<uint64_t> claim_{0};      // (job generation << 32) | next piece index
+  std::atomic<int> active_[2] = {{0}, {0}};  // threads inside a job of slot (generation & 1)
+  std::atomic<int> pending_{0}, sleepers_{0};
   std::atomic<bool> stop_{false};
 };
 

@@ -485,3 +485,92 @@ def test_filter_stage_groups_bitwise(orc, cp, prec):
     for o in outs[5:]:  # other tile configurations: same tolerance, not the same bits
         assert per_output_error(o, ref, orc.output_scale(F, I, cp)) <= TOL[prec]
     assert per_output_error(outs[0], ref, orc.output_scale(F, I, cp)) <= TOL[prec]
+
+
+# ---------------------------------------------------------------- workspace semantics
+def test_workspace_limit_checked_on_every_call(orc):
+    """ScratchTracker::allocate checks the limit on every claim (scratch.cpp:15-19): a
+    cached larger buffer must not let an oversized explicit call through, and
+    current/peak count claims, not the cached allocation."""
+    cp = dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=40, w_i=40, b=4, s=1, p=1)
+    F, I = rand_inputs(cp, 61)
+    dF, dI = to_dev(F), to_dev(I)
+    need = cg.conv_workspace_bytes(cp, "explicit", "tf32")
+    cg.conv(dF, dI, cp, algo="explicit", precision="tf32")  # caches a buffer >= need
+    torch.cuda.synchronize()
+    assert cg.lib.cgb_scratch_cached_bytes() >= need
+    assert cg.lib.cgb_scratch_current_bytes() == 0  # claims end with the call
+    cg.scratch_set_limit(need - 1)
+    try:
+        with pytest.raises(cg.AllocationFailure):
+            cg.conv(dF, dI, cp, algo="explicit", precision="tf32")
+        cg.conv(dF, dI, cp, algo="fused", precision="tf32")  # no workspace: still runs
+    finally:
+        cg.scratch_set_limit(0)
+    cg.scratch_reset_peak()
+    cg.conv(dF, dI, cp, algo="fused", precision="tf32")
+    assert cg.scratch_peak_bytes() == 0
+    cg.conv(dF, dI, cp, algo="explicit", precision="tf32")
+    assert cg.scratch_peak_bytes() == need
+
+
+def test_workspace_per_stream_concurrent(orc):
+    """3xTF32 writes its filter split into workspace: calls on two streams with different
+    filters, enqueued back to back, must not share (and overwrite) one buffer."""
+    cp = dict(k_n=128, k_h=3, k_w=3, c_i=64, h_i=28, w_i=28, b=8, s=1, p=1)
+    Fa, I = rand_inputs(cp, 71)
+    Fb, _ = rand_inputs(cp, 72)
+    dFa, dFb, dI = to_dev(Fa), to_dev(Fb), to_dev(I)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            oa = cg.conv(dFa, dI, cp, precision="3xtf32")
+        with torch.cuda.stream(s2):
+            ob = cg.conv(dFb, dI, cp, precision="3xtf32")
+        outs.append((oa, ob))
+    torch.cuda.synchronize()
+    for F, k in ((Fa, 0), (Fb, 1)):
+        ref = orc.conv_gemm(F, I, cp)
+        for o in outs:
+            assert per_output_error(to_host(o[k]), ref, orc.output_scale(F, I, cp)) <= 1e-5
+
+
+def test_workspace_growth_keeps_captured_buffer(orc):
+    """A graph captured with the cached workspace keeps working after a later call on the
+    same stream needs (and allocates) a bigger one: captured buffers are never freed."""
+    cp = dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=16, w_i=16, b=2, s=1, p=1)
+    big = dict(k_n=256, k_h=3, k_w=3, c_i=256, h_i=14, w_i=14, b=2, s=1, p=1)
+    F, I = rand_inputs(cp, 81)
+    Fb, Ib = rand_inputs(big, 82)
+    dF, dI, dFb, dIb = to_dev(F), to_dev(I), to_dev(Fb), to_dev(Ib)
+    cg.lib.cgb_scratch_release()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        O = cg.conv(dF, dI, cp, precision="3xtf32")  # allocates this stream's workspace
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            cg.conv(dF, dI, cp, precision="3xtf32", out=O)
+        cg.conv(dFb, dIb, big, precision="3xtf32")  # outgrows the captured buffer
+        st.synchronize()
+        O.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    ref = orc.conv_gemm(F, I, cp)
+    assert per_output_error(to_host(O), ref, orc.output_scale(F, I, cp)) <= 1e-5
+
+
+def test_host_pipeline_pageable_stress():
+    """The pageable-buffer path (pinned bounce ring + parallel memcpy pool) over many small
+    chunks, repeated: every repetition bit-identical to the device path."""
+    cp = dict(k_n=32, k_h=3, k_w=3, c_i=64, h_i=32, w_i=32, b=96, s=1, p=1)
+    F, I = rand_inputs(cp, 91)
+    dev = to_host(cg.conv(to_dev(F), to_dev(I), cp, precision="tf32"))
+    # 10 images (2.5 MB of input) per chunk: ~10 chunks, more than the bounce slots, each
+    # copy large enough (>= 2 MiB) for the parallel memcpy pool
+    with cg.tuning(host_chunk_kb=2560):
+        for _ in range(20):
+            out = np.zeros_like(dev, order="F")
+            cg.conv(F, I, cp, precision="tf32", out=out)
+            assert np.array_equal(out, dev)
