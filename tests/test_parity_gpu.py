@@ -562,15 +562,22 @@ def test_workspace_growth_keeps_captured_buffer(orc):
 
 
 def test_host_pipeline_pageable_stress():
-    """The pageable-buffer path (pinned bounce ring + parallel memcpy pool) over many small
-    chunks, repeated: every repetition bit-identical to the device path."""
+    """The pageable-buffer path (pinned bounce ring + parallel memcpy pool) over many
+    chunks, repeated: every repetition bit-identical, and equal to the device path."""
     cp = dict(k_n=32, k_h=3, k_w=3, c_i=64, h_i=32, w_i=32, b=96, s=1, p=1)
     F, I = rand_inputs(cp, 91)
     dev = to_host(cg.conv(to_dev(F), to_dev(I), cp, precision="tf32"))
     # 10 images (2.5 MB of input) per chunk: ~10 chunks, more than the bounce slots, each
     # copy large enough (>= 2 MiB) for the parallel memcpy pool
+    # (chunks are b=10 convolutions, which may take other tile splits than the b=96 launch:
+    # repetitions are compared bitwise with each other and with the device path in tolerance)
     with cg.tuning(host_chunk_kb=2560):
+        first = None
         for _ in range(20):
             out = np.zeros_like(dev, order="F")
             cg.conv(F, I, cp, precision="tf32", out=out)
-            assert np.array_equal(out, dev)
+            if first is None:
+                first = out
+                scale = np.abs(dev).max()
+                assert np.max(np.abs(out - dev)) <= 1e-5 * scale
+            assert np.array_equal(out, first)
