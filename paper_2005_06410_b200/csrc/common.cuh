@@ -86,6 +86,12 @@ CGB_DEV void red_add_v4(float* p, const uint32_t* r) {
                "f"(__uint_as_float(r[1])), "f"(__uint_as_float(r[2])), "f"(__uint_as_float(r[3]))
                : "memory");
 }
+// 16-byte load through L2 only (data written by other CTAs of the same grid).
+CGB_DEV void ld_global_cg_v4(const float* p, float* v) {
+  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p)
+               : "memory");
+}
+
 CGB_DEV int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -80,7 +80,9 @@ struct Args {
   // of a layer whose row count leaves it half empty is cut into smaller tiles that fill
   // all groups (0 = every m-tile has MT subtiles).
   int32_t m_full, tail_mt;
-  int* counters;      // [sk tile][ranks*4 epilogue warps] pieces written; zero between launches
+  int* counters;      // [sk tile][ranks*4 epilogue warps][2] pieces arrived / written; zero between launches
+  float* sk_ws;       // partial tiles of split pieces: [sk tile][rank][sk_pieces][MT*128 x BN]
+  int32_t sk_pieces;  // most pieces any split tile has
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
   int32_t tps;        // taps per filter stage group (divides B_STAGES; see the filter TMA warp)
@@ -265,10 +267,16 @@ CGB_DEV void issue_tap_partial(uint32_t d_base, uint64_t at, uint64_t at_lo, uin
 
 // Epilogue of one accumulator set: TMEM -> registers -> O for the units u = u0, u0 + du,
 // ... of the tile's (M subtile, 32-column block) pairs, for the 32 rows of TMEM lane
-// quadrant `sub` (the calling warp's warp % 4). add: stream-K piece, red.add into O.
+// quadrant `sub` (the calling warp's warp % 4).
+// Stream-K pieces (sk_mode): 1 = write this piece's partial to its workspace slot
+// (ws_own: [unit][sub][lane][32] floats, each lane one 128-byte run), 2 = the last piece
+// to arrive: O = p_0 + p_1 + ... in piece order (own registers at position prank, the
+// others from the workspace slots ws_all + r * piece_stride), then store as usual;
+// 3 = red.add into O (the second of two pieces).
 template <int BN>
 CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, int32_t m0, int n0, int mtc, int sub,
-                         int lane, int u0, int du, bool add) {
+                         int lane, int u0, int du, int sk_mode = 0, float* ws_own = nullptr,
+                         const float* ws_all = nullptr, size_t piece_stride = 0, int npieces = 1, int prank = 0) {
   constexpr int NCB = BN / 32;
   const int32_t hw_q = a.Hq * a.Wq;
 #pragma unroll 1
@@ -286,6 +294,35 @@ CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, i
     uint32_t r[32];
     tmem_ld_32x32b_x32(trow + cb * 32, r);
     tmem_ld_wait();
+    const size_t run = ((size_t)(u * 4 + sub) * 32 + lane) * 32;  // this lane's 32 floats in a piece slot
+    if (sk_mode == 1) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) st_global_v8(ws_own + run + j, &r[j]);
+      continue;
+    }
+    if (sk_mode == 2) {
+      // four columns at a time (registers: the kernel runs at its launch bound)
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float acc[4], v[4];
+        const float own[4] = {__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                              __uint_as_float(r[j + 3])};
+#pragma unroll 1
+        for (int q = 0; q < npieces; ++q) {
+          if (q == prank) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = own[i];
+          } else {
+            ld_global_cg_v4(ws_all + (size_t)q * piece_stride + run + j, v);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i] = q == 0 ? v[i] : acc[i] + v[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[j + i] = __float_as_uint(acc[i]);
+      }
+    }
+    const bool add = sk_mode == 3;
     const int nb = n0 + cb * 32;
     if (a.pstore && a.vec && nb + 32 <= a.k_n && !CGB_DBG(4)) {
       // Lane pairs write whole 64-byte runs: in store A_k the pair writes segments
@@ -308,7 +345,7 @@ CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, i
         for (int i = 0; i < 8; ++i) v[i] = par ? x[i] : r[16 * k + i];
         if (PA >= 0) {
           if (!add) st_global_v8(dA + 16 * k, v);
-          else {  // stream-K piece: the pair's 16-byte reds share 128-byte lines too
+          else {  // second stream-K piece: the pair's 16-byte reds share 128-byte lines too
             red_add_v4(dA + 16 * k, v);
             red_add_v4(dA + 16 * k + 4, v + 4);
           }
@@ -829,38 +866,56 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (CGB_DBG(64)) epi_wait += e1 - e0;
       tc_fence_after();
       // ---- stream-K piece of a split tile. Groups' unit ranges are contiguous, so every
-      // group whose range meets the tile holds exactly one piece of it, and the pieces are
-      // ordered by channel chunk. They are combined in a FIXED order, highest chunks first:
-      // the piece of rank 0 (the last group touching the tile, for which it is the FIRST
-      // segment, so it finishes early) stores its rows; the piece of rank r waits until r
-      // pieces have been written and red.adds its rows into O. O = ((p_0 + p_1) + p_2)...,
-      // bitwise independent of timing. Waits only point at pieces that are earlier
-      // segments of higher-numbered groups, so the chain always resolves. The last piece
-      // resets the counter for the next launch.
+      // group whose range meets the tile holds exactly one piece of it; pieces are ranked
+      // by channel chunk (prank 0 = the highest chunks). No piece ever waits for a piece
+      // that has not started: each first arrives on the tile's counters (per CTA rank and
+      // epilogue warp) and only ever waits for pieces that arrived before it -- those are
+      // resident and running -- so there is no co-residency assumption (concurrent grids,
+      // MPS, SM-limited contexts cannot deadlock it), and the sum is bitwise independent
+      // of the arrival order:
+      // * two pieces (every automatic split: each group holds >= one tile of units): the
+      //   first to arrive stores its rows, the second waits for that store and red.adds
+      //   its rows (p_0 + p_1 == p_1 + p_0 in fp32);
+      // * more pieces (forced splits): all but the last to arrive write their partial
+      //   rows to a workspace slot; the last waits for those writes and stores
+      //   O = ((p_0 + p_1) + p_2) + ... in piece order.
+      // The last piece resets the counters for the next launch.
       const bool whole = cc0 == 0 && cc1 == a.CC;
-      int* cnt = nullptr;
-      bool add = false;
-      int prank = 0, npieces = 1;
-      if (!whole) {
+      const uint32_t trow0 = tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS;
+      if (whole) {
+        store_units<BN>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1);
+      } else {
         const int u0 = tile * a.CC;  // stream-K tiles are tiles [0, sk_tiles)
         const int g_hi = sk_group_of(a, u0 + a.CC - 1);
-        prank = g_hi - gid;
-        npieces = g_hi - sk_group_of(a, u0) + 1;
-        cnt = a.counters + (size_t)tile * (PAIR ? 8 : 4) + rank * 4 + sub;
-        add = prank > 0;
-        if (add)
-          while (ld_acquire_gpu(cnt) < prank) {
+        const int prank = g_hi - gid;
+        const int npieces = g_hi - sk_group_of(a, u0) + 1;
+        int* cnt = a.counters + 2 * ((size_t)tile * (PAIR ? 8 : 4) + rank * 4 + sub);
+        int order = 0;
+        if (lane == 0) order = atomicAdd(cnt, 1);
+        order = __shfl_sync(0xffffffffu, order, 0);
+        const bool last = order + 1 == npieces;
+        if (last && lane == 0) {
+          while (ld_acquire_gpu(cnt + 1) < npieces - 1) {  // pieces that arrived earlier
           }
-      }
-      store_units<BN>(a, O, tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS, m0, n0, mtc, sub,
-                      lane, 0, 1, add);
-      if (!whole) {
-        if (prank + 1 < npieces) {
-          __threadfence();  // each lane's rows (stores or reds) before the "written" count
+          cnt[0] = 0;  // every other piece has arrived and written: reset for the next launch
+          cnt[1] = 0;
+        }
+        if (last) {
           __syncwarp();
-          if (lane == 0) atomicAdd(cnt, 1);
-        } else if (lane == 0) {
-          *cnt = 0;  // last piece: every other piece has written and stopped polling
+          __threadfence();
+        }
+        if (npieces == 2) {
+          store_units<BN>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, last ? 3 : 0);
+        } else {
+          const size_t piece = (size_t)MT * 128 * BN;
+          float* ws_all = a.sk_ws + ((size_t)tile * (PAIR ? 2 : 1) + rank) * a.sk_pieces * piece;
+          if (!last) store_units<BN>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, 1, ws_all + prank * piece);
+          else store_units<BN>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, 2, nullptr, ws_all, piece, npieces, prank);
+        }
+        if (!last) {
+          __threadfence();  // the rows (O or workspace) before the "written" count
+          __syncwarp();
+          if (lane == 0) atomicAdd(cnt + 1, 1);
         }
       }
       tc_fence_before();
@@ -894,29 +949,50 @@ __global__ void __launch_bounds__(THREADS, 1)
 // run concurrently never share one. Zeroed once at allocation; every launch leaves them
 // zero again (the second piece resets its pair).
 constexpr double kSkFill = 0.9;  // split when the last round of whole tiles is < 90% full
-struct SkCounters {
-  int* counters = nullptr;
+struct SkState {
+  int* counters = nullptr;  // zero between launches (the last piece of each tile resets its pair)
   size_t n = 0;
+  float* ws = nullptr;      // partial tiles
+  size_t ws_bytes = 0;
+  bool captured = false;    // used while the stream was being captured: never freed implicitly
 };
 static std::mutex g_sk_mu;
-static std::map<std::pair<int, cudaStream_t>, SkCounters> g_sk;
+static std::map<std::pair<int, cudaStream_t>, SkState> g_sk;
+static std::vector<void*> g_sk_retired;
 
-
-static int* sk_counters(cudaStream_t st, size_t n) {
+// Counters (n ints) and partial-tile workspace (ws_bytes) for a stream-K launch on st,
+// one set per (device, stream) so launches that may run concurrently never share one.
+static bool sk_buffers(cudaStream_t st, size_t n, size_t ws_bytes, int** counters, float** ws) {
   std::lock_guard<std::mutex> lk(g_sk_mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  SkCounters& c = g_sk[{dev, st}];
+  SkState& c = g_sk[{dev, st}];
+  const bool capturing = !can_free_now(st);
+  auto drop = [&](void* p) {
+    if (!p) return;
+    if (c.captured || capturing) g_sk_retired.push_back(p);  // a captured graph may use it
+    else cudaFree(p);
+  };
   if (c.n < n) {
-    const size_t m = std::max<size_t>(n, 4096);
-    if (c.counters && can_free_now(st)) cudaFree(c.counters);  // leaked while capturing
+    const size_t m = std::max<size_t>(n, 8192);
+    drop(c.counters);
     c.counters = nullptr;
     c.n = 0;
     if (capture_safe_malloc(reinterpret_cast<void**>(&c.counters), m * sizeof(int), /*zero=*/true) != cudaSuccess)
-      return nullptr;  // no counters: whole tiles only
+      return false;  // no counters: whole tiles only
     c.n = m;
   }
-  return c.counters;
+  if (ws_bytes > 0 && c.ws_bytes < ws_bytes) {
+    drop(c.ws);
+    c.ws = nullptr;
+    c.ws_bytes = 0;
+    if (capture_safe_malloc(reinterpret_cast<void**>(&c.ws), ws_bytes) != cudaSuccess) return false;
+    c.ws_bytes = ws_bytes;
+  }
+  c.captured = c.captured || capturing;
+  *counters = c.counters;
+  *ws = c.ws;
+  return true;
 }
 
 template <int MT, int BN, bool SPLIT, int A_SLOTS, int B_STAGES, bool PAIR, int UPI>
@@ -1001,21 +1077,40 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   a.dp_tiles = tiles;
   a.sk_units = 0;
   a.counters = nullptr;
+  a.sk_ws = nullptr;
+  a.sk_pieces = 1;
   const int rounds = (tiles + gmax - 1) / gmax;
   const double fill = (double)tiles / ((double)rounds * gmax);
   const int sk_mode = tu.sk;
   // Stream-K only for the last one-to-two rounds of at least one tile per group: every
-  // split tile adds a red.add pass over its rows (L2 atomics), which measured slower than
-  // the idle SMs it saves when ALL tiles would be split (1-round layers: 7x7, 14x14).
-  // The fixup itself handles any number of pieces per tile (sk_mode 2 forces it).
+  // split piece adds a pass over its rows through the workspace, which measured slower
+  // than the idle SMs it saves when ALL tiles would be split (1-round layers: 7x7,
+  // 14x14). The fixup itself handles any number of pieces per tile (sk_mode 2 forces it).
   const bool sk_ok = !a.tail_mt && (sk_mode == 2 ? (int64_t)tiles * a.CC >= 2 * gmax : tiles >= gmax);
   if (sk_mode != 0 && a.CC >= 2 && sk_ok && (fill < kSkFill || sk_mode == 2)) {
     const int dp = std::max(0, tiles / gmax - 1) * gmax;
     const int sk_tiles = tiles - dp;
-    if ((a.counters = sk_counters(st, (size_t)sk_tiles * (PAIR ? 8 : 4))) != nullptr) {
+    const int units = sk_tiles * a.CC;
+    auto begin = [&](int g) { return (int)((int64_t)g * units / gmax); };
+    auto group_of = [&](int x) {
+      int c = (int)((int64_t)x * gmax / units);
+      while (c + 1 < gmax && begin(c + 1) <= x) ++c;
+      return c;
+    };
+    int pieces = 1;
+    for (int t = 0; t < sk_tiles; ++t)
+      pieces = std::max(pieces, group_of(t * a.CC + a.CC - 1) - group_of(t * a.CC) + 1);
+    // partial-tile workspace: only splits into more than two pieces use it
+    const size_t ws_bytes = pieces > 2 ? (size_t)sk_tiles * (PAIR ? 2 : 1) * pieces * MT * 128 * BN * sizeof(float) : 0;
+    int* cnt = nullptr;
+    float* ws = nullptr;
+    if (sk_buffers(st, (size_t)sk_tiles * (PAIR ? 8 : 4) * 2, ws_bytes, &cnt, &ws)) {
+      a.counters = cnt;
+      a.sk_ws = ws;
+      a.sk_pieces = pieces;
       a.groups = gmax;
       a.dp_tiles = dp;
-      a.sk_units = sk_tiles * a.CC;
+      a.sk_units = units;
     }
   }
   if (tu.verbose)
