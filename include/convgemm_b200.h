@@ -59,10 +59,14 @@ typedef enum cgb_status {
     CGB_UNSUPPORTED = 6         /* e.g. f64 requested on the device path */
 } cgb_status;
 
-/* Operator selection: the reference's Algo::Im2col vs Algo::ConvGemm (bench.hpp:13-19). */
+/* Operator selection: the reference's Algo::Im2col / Algo::ConvGemm / Algo::Direct
+ * (bench.hpp:13-19; conv.hpp:24-91). */
 typedef enum cgb_algo {
     CGB_ALGO_EXPLICIT = 0, /* im2col kernel writes B-hat to HBM, then the GEMM kernel */
-    CGB_ALGO_FUSED = 1     /* implicit GEMM: B-hat tiles gathered straight into shared memory */
+    CGB_ALGO_FUSED = 1,    /* implicit GEMM: B-hat tiles gathered straight into shared memory */
+    CGB_ALGO_DIRECT = 2    /* conv_direct: the seven-loop convolution, bit-identical to the
+                              reference's (fp32 product then add, its loop order); precision
+                              is ignored. The checker, not a fast path. */
 } cgb_algo;
 
 /* Arithmetic on the tensor cores (or CUDA cores). */
@@ -110,11 +114,35 @@ cgb_status cgb_im2col(const float* I, const cgb_conv_params* cp, float* B, int64
 cgb_status cgb_gemm(int precision, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                     int64_t m, int64_t n, int64_t k, void* workspace, size_t workspace_bytes, void* stream);
 
-/* ---- host-pointer entry point: synchronous, reference semantics ----
+/* ---- host-pointer entry points: synchronous, reference semantics ----
  * Copies F and I host->device, runs cgb_conv, copies O device->host, syncs.
  * Host buffers may be pageable or pinned. */
 cgb_status cgb_conv_host(int algo, int precision, const float* F_host, const float* I_host,
                          const cgb_conv_params* cp, float* O_host, void* stream);
+/* im2col<float> (im2col.hpp:77-120) on host buffers: B_host (k x n, leading dimension
+ * ldb >= k) written bit-identically to the reference's lowered matrix. */
+cgb_status cgb_im2col_host(const float* I_host, const cgb_conv_params* cp, float* B_host, int64_t ldb);
+/* gemm (gemm.hpp:46-105) on host buffers: C (+)= A * B for column-major A (m x k, lda),
+ * B (k x n, ldb), C (m x n, ldc). accumulate != 0 adds to C like the reference's gemm
+ * (which callers precede with zero_matrix); 0 overwrites C. */
+cgb_status cgb_gemm_host(int precision, const float* A_host, int64_t lda, const float* B_host, int64_t ldb,
+                         float* C_host, int64_t ldc, int64_t m, int64_t n, int64_t k, int accumulate);
+
+/* ---- float64: the reference's f64 instantiations (bindings.cpp:58-65) on the device ----
+ * Bit-identical to the reference's conv_direct<double> / conv_gemm<double> /
+ * conv_im2col_gemm<double> / im2col<double> / gemm<double>: the reference's
+ * accumulation order (kc-blocked, kc from bp; bp may be NULL = BlockingParams{}) with
+ * every product rounded before its add, on FP64 CUDA cores. A checker and a
+ * compatibility path, not the performance path. cgb_conv_f64 takes device pointers (on
+ * `stream`); the *_host_f64 calls take host pointers and are synchronous. */
+cgb_status cgb_conv_f64(int algo, const double* F, const double* I, const cgb_conv_params* cp,
+                        const cgb_blocking_params* bp, double* O, void* stream);
+cgb_status cgb_conv_host_f64(int algo, const double* F_host, const double* I_host, const cgb_conv_params* cp,
+                             const cgb_blocking_params* bp, double* O_host);
+cgb_status cgb_im2col_host_f64(const double* I_host, const cgb_conv_params* cp, double* B_host, int64_t ldb);
+cgb_status cgb_gemm_host_f64(const double* A_host, int64_t lda, const double* B_host, int64_t ldb, double* C_host,
+                             int64_t ldc, int64_t m, int64_t n, int64_t k, const cgb_blocking_params* bp,
+                             int accumulate);
 
 /* ---- workspace accounting (ScratchTracker equivalent, scratch.hpp:14-28) ----
  * Every call that needs device workspace (and was given none) claims its size: the

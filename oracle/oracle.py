@@ -152,6 +152,8 @@ class Reference:
         lib.ref_gemm_dims.argtypes = [_i64p, _i64p, _i64p, _i64p]
         lib.ref_im2col_f32.argtypes = [_vp, _i64p, ctypes.c_int, _vp]
         lib.ref_gemm_f32.argtypes = [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i64p, ctypes.c_int]
+        lib.ref_gemm_f64.argtypes = [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i64p, ctypes.c_int]
+        lib.ref_im2col_f64.argtypes = [_vp, _i64p, ctypes.c_int, _vp]
         lib.ref_im2col_workspace_bytes.argtypes = [_i64p]
         lib.ref_im2col_workspace_bytes.restype = ctypes.c_int64
         lib.ref_convgemm_scratch_bytes.argtypes = [_i64p]
@@ -202,9 +204,24 @@ class Reference:
     def im2col(self, I, cp, threads=1):
         a = list(_cp_array(cp))
         h_o, w_o = output_dims_py(cp)
-        B = np.zeros((a[1] * a[2] * a[3], h_o * w_o * a[6]), dtype=np.float32, order="F")
-        self._check(self.lib.ref_im2col_f32(_ptr(I), _cp_array(cp), threads, _ptr(B)))
+        f64 = I.dtype == np.float64
+        B = np.zeros((a[1] * a[2] * a[3], h_o * w_o * a[6]), dtype=np.float64 if f64 else np.float32, order="F")
+        fn = self.lib.ref_im2col_f64 if f64 else self.lib.ref_im2col_f32
+        self._check(fn(_ptr(I), _cp_array(cp), threads, _ptr(B)))
         return B
+
+    def gemm(self, A, B, bp=None, threads=1):
+        """Column-major C = A @ B through the reference's blocked gemm (gemm.hpp:46-105)."""
+        f64 = A.dtype == np.float64
+        A = np.asfortranarray(A, dtype=np.float64 if f64 else np.float32)
+        B = np.asfortranarray(B, dtype=A.dtype)
+        m, k = A.shape
+        n = B.shape[1]
+        C = np.zeros((m, n), dtype=A.dtype, order="F")
+        bpa = (ctypes.c_int64 * 5)(*bp) if bp is not None else None
+        fn = self.lib.ref_gemm_f64 if f64 else self.lib.ref_gemm_f32
+        self._check(fn(_ptr(A), _ptr(B), _ptr(C), m, n, k, bpa, threads))
+        return C
 
     # --- the reference tests' generators (proj/tests/oracles.hpp:48-91) ---
     def rng(self, seed: int) -> "RefRng":

@@ -120,6 +120,25 @@ int ref_im2col_f32(const float* I, const int64_t* cpa, int threads, float* B) {
     });
 }
 
+int ref_im2col_f64(const double* I, const int64_t* cpa, int threads, double* B) {
+    return guarded([&] {
+        const ConvParams cp = to_cp(cpa);
+        Tensor4View<const double> Iv{I, cp.h_i, cp.w_i, cp.c_i, cp.b};
+        const Im2colMatrix<double> m = im2col<double>(Iv, cp, threads);
+        std::copy_n(m.view().data, m.rows() * m.cols(), B);
+    });
+}
+
+int ref_gemm_f64(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k,
+                 const int64_t* bp, int threads) {
+    return guarded([&] {
+        MatrixView<double> Cv{C, m, n, m};
+        zero_matrix(Cv);
+        gemm<double>(MatrixView<const double>{A, m, k, m}, MatrixView<const double>{B, k, n, k}, Cv,
+                     to_bp(bp), threads);
+    });
+}
+
 // Column-major C = A*B (m x k times k x n), reference blocked gemm.
 int ref_gemm_f32(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
                  const int64_t* bp, int threads) {

@@ -30,16 +30,16 @@ __all__ = [
     "AllocationFailure", "BlockingParams", "ConvParams", "DimensionMismatch", "InvalidGeometry",
     "conv", "conv_gemm", "conv_im2col_gemm", "convgemm_scratch_bytes", "empty_tensor4", "gemm_dims",
     "im2col", "im2col_workspace_bytes", "output_dims", "scratch_peak_bytes", "scratch_reset_peak",
-    "scratch_set_limit", "kernel_launch_count", "last_path", "PRECISIONS", "ALGOS", "gemm",
+    "scratch_set_limit", "kernel_launch_count", "last_path", "PRECISIONS", "ALGOS", "gemm", "conv_direct",
     "set_tuning", "get_tuning", "tuning",
     "IoError", "conv_workspace_bytes", "LayerSpec", "ModelSpec", "LayerResult", "ParseError", "UnknownLayerKind", "parse_model",
     "model_workspace_bytes", "run_inference", "write_csv",
 ]
 
-ALGOS = {"explicit": 0, "im2col": 0, "fused": 1, "convgemm": 1}
+ALGOS = {"explicit": 0, "im2col": 0, "fused": 1, "convgemm": 1, "direct": 2}
 PRECISIONS = {"auto": 0, "3xtf32": 1, "tf32": 2, "ffma": 3}
 PATHS = {0: "none", 1: "tcgen05-implicit", 2: "tcgen05-explicit", 3: "ffma-implicit", 4: "ffma-explicit",
-         5: "tcgen05-shifted", 6: "tcgen05-gather", 7: "tcgen05-shifted-wim"}
+         5: "tcgen05-shifted", 6: "tcgen05-gather", 7: "tcgen05-shifted-wim", 8: "direct"}
 
 
 class InvalidGeometry(ValueError):
@@ -215,12 +215,12 @@ def _expect_shape(x, shape, name):
         raise InvalidGeometry(f"{name} tensor extents {tuple(x.shape)} disagree with ConvParams {tuple(shape)}")
 
 
-def _torch_ptr(x, name, writable=False):
+def _torch_ptr(x, name, writable=False, dtype=None):
     import torch
     if not x.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (or a numpy array for the host path)")
-    if x.dtype != torch.float32:
-        raise Unsupported(f"{name}: only float32 runs on the device path (got {x.dtype})")
+    if x.dtype != (dtype or torch.float32):
+        raise Unsupported(f"{name}: expected {dtype or torch.float32} on this path (got {x.dtype})")
     d = x.shape
     expect = (1, d[0], d[0] * d[1], d[0] * d[1] * d[2])
     if x.dim() != 4 or (x.numel() > 0 and tuple(x.stride()) != expect):
@@ -233,19 +233,32 @@ def _shapes(cp: ConvParams):
     return ((cp.k_n, cp.k_h, cp.k_w, cp.c_i), (cp.h_i, cp.w_i, cp.c_i, cp.b), (cp.k_n, h_o, w_o, cp.b))
 
 
-def conv(F, I, cp, algo: str = "fused", precision: str = "auto", out=None, stream=None, workspace=None):
-    """O = CONV(F, I). ``algo`` in {"fused", "explicit"} (bench.hpp:13-19: ConvGemm vs Im2col)."""
+def conv(F, I, cp, algo: str = "fused", precision: str = "auto", out=None, stream=None, workspace=None,
+         blocking: BlockingParams | None = None):
+    """O = CONV(F, I). ``algo`` in {"fused", "explicit", "direct"} (bench.hpp:13-19:
+    ConvGemm, Im2col, Direct). float32 runs the B200 operator (``precision``); float64
+    (numpy or torch) runs the reference's f64 arithmetic bit for bit on the device's
+    FP64 cores (``blocking.kc`` sets the accumulation blocks, as in the reference)."""
     cp = ConvParams.of(cp)
     fs, is_, os_ = _shapes(cp)
     a, p = ALGOS[algo], PRECISIONS[precision]
+    bp = ctypes.byref(blocking.c()) if blocking is not None else None
     if _is_torch(F):
         import torch
         _expect_shape(F, fs, "filter")
         _expect_shape(I, is_, "input")
+        f64 = F.dtype == torch.float64
+        if f64 != (I.dtype == torch.float64):
+            raise Unsupported("filter and input must have the same dtype")
         if out is None:
-            out = empty_tensor4(*os_, device=F.device)
+            out = empty_tensor4(*os_, device=F.device, dtype=F.dtype)
         _expect_shape(out, os_, "output")
         st = stream if stream is not None else torch.cuda.current_stream(F.device).cuda_stream
+        if f64:
+            _check(lib.cgb_conv_f64(a, _torch_ptr(F, "filter", dtype=torch.float64),
+                                    _torch_ptr(I, "input", dtype=torch.float64), ctypes.byref(cp.c()), bp,
+                                    _torch_ptr(out, "output", dtype=torch.float64), st))
+            return out
         ws_ptr, ws_bytes = (workspace.data_ptr(), workspace.numel() * workspace.element_size()) \
             if workspace is not None else (None, 0)
         _check(lib.cgb_conv(a, p, _torch_ptr(F, "filter"), _torch_ptr(I, "input"), ctypes.byref(cp.c()),
@@ -253,17 +266,18 @@ def conv(F, I, cp, algo: str = "fused", precision: str = "auto", out=None, strea
         return out
     # host path: numpy arrays (reference semantics, synchronous)
     dt = np.float64 if (np.asarray(F).dtype == np.float64 or np.asarray(I).dtype == np.float64) else np.float32
-    if dt == np.float64:
-        raise Unsupported("float64 runs on the CPU reference only; the B200 operator is float32")
-    F = np.asfortranarray(F, dtype=np.float32)
-    I = np.asfortranarray(I, dtype=np.float32)
+    F = np.asfortranarray(F, dtype=dt)
+    I = np.asfortranarray(I, dtype=dt)
     _expect_shape(F, fs, "filter")
     _expect_shape(I, is_, "input")
     if out is None:
-        out = np.empty(os_, dtype=np.float32, order="F")
+        out = np.empty(os_, dtype=dt, order="F")
     _expect_shape(out, os_, "output")
-    if not out.flags.f_contiguous or out.dtype != np.float32:
-        raise ValueError("output must be a Fortran-ordered float32 array")
+    if not out.flags.f_contiguous or out.dtype != dt:
+        raise ValueError(f"output must be a Fortran-ordered {np.dtype(dt).name} array")
+    if dt == np.float64:
+        _check(lib.cgb_conv_host_f64(a, F.ctypes.data, I.ctypes.data, ctypes.byref(cp.c()), bp, out.ctypes.data))
+        return out
     _check(lib.cgb_conv_host(a, p, F.ctypes.data, I.ctypes.data, ctypes.byref(cp.c()), out.ctypes.data, None))
     return out
 
@@ -277,14 +291,20 @@ def conv_gemm(F, I, cp, blocking: BlockingParams | None = None, threads: int = 1
               out=None):
     """Fused ConvGemm (conv.hpp:78-91): im2col happens inside the operand staging."""
     _validate_blocking(blocking)
-    return conv(F, I, cp, "fused", precision, out)
+    return conv(F, I, cp, "fused", precision, out, blocking=blocking)
 
 
 def conv_im2col_gemm(F, I, cp, blocking: BlockingParams | None = None, threads: int = 1, precision: str = "auto",
                      out=None):
     """Explicit im2col + GEMM (conv.hpp:60-74): B-hat is materialised in HBM."""
     _validate_blocking(blocking)
-    return conv(F, I, cp, "explicit", precision, out)
+    return conv(F, I, cp, "explicit", precision, out, blocking=blocking)
+
+
+def conv_direct(F, I, cp, out=None):
+    """The reference's seven-loop convolution (conv.hpp:24-55) on the device, bit-identical
+    to the reference's conv_direct<float> / <double>: the checker of run_inference."""
+    return conv(F, I, cp, "direct", "auto", out)
 
 
 def gemm(A, B, blocking: BlockingParams | None = None, threads: int = 1, precision: str = "auto", out=None):
@@ -298,7 +318,17 @@ def gemm(A, B, blocking: BlockingParams | None = None, threads: int = 1, precisi
     if host:
         An, Bn = np.asarray(A), np.asarray(B)
         if An.dtype == np.float64 or Bn.dtype == np.float64:
-            raise Unsupported("float64 runs on the CPU reference only; the B200 operator is float32")
+            # the reference's gemm<double> bit for bit on the device's FP64 cores
+            An = np.asfortranarray(An, dtype=np.float64)
+            Bn = np.asfortranarray(Bn, dtype=np.float64)
+            if An.ndim != 2 or Bn.ndim != 2 or An.shape[1] != Bn.shape[0]:
+                raise DimensionMismatch("gemm operand extents disagree")
+            m, k = An.shape
+            n = Bn.shape[1]
+            C = np.zeros((m, n), dtype=np.float64, order="F")
+            bp = ctypes.byref(blocking.c()) if blocking is not None else None
+            _check(lib.cgb_gemm_host_f64(An.ctypes.data, m, Bn.ctypes.data, k, C.ctypes.data, m, m, n, k, bp, 0))
+            return C
         A = torch.from_numpy(np.ascontiguousarray(An.astype(np.float32).T)).cuda().t()
         B = torch.from_numpy(np.ascontiguousarray(Bn.astype(np.float32).T)).cuda().t()
     if A.dim() != 2 or B.dim() != 2:
@@ -324,13 +354,20 @@ def gemm(A, B, blocking: BlockingParams | None = None, threads: int = 1, precisi
 
 
 def im2col(I, cp, threads: int = 1, ldb: int | None = None, out=None):
-    """Lowered matrix B (k x n, column-major) from the device kernel; bit-exact with im2col<float>."""
+    """Lowered matrix B (k x n, column-major) from the device kernel; bit-exact with im2col<float>
+    (and im2col<double> for float64 input)."""
     import torch
     cp = ConvParams.of(cp)
     _, is_, _ = _shapes(cp)
     _, n, k = gemm_dims(cp)
     ldb = k if ldb is None else ldb
     host = not _is_torch(I)
+    if host and np.asarray(I).dtype == np.float64:
+        In = np.asfortranarray(I, dtype=np.float64)
+        _expect_shape(In, is_, "input")
+        B = np.zeros((ldb, n), dtype=np.float64, order="F")
+        _check(lib.cgb_im2col_host_f64(In.ctypes.data, ctypes.byref(cp.c()), B.ctypes.data, ldb))
+        return B[:k]
     if host:
         I = torch.from_numpy(np.asfortranarray(I, dtype=np.float32).reshape(-1, order="F")).cuda()
         I = I.view(cp.b, cp.c_i, cp.w_i, cp.h_i).permute(3, 2, 1, 0)

@@ -20,7 +20,8 @@ SYMBOLS = (
     "cgb_gemm", "cgb_conv_host", "cgb_scratch_current_bytes", "cgb_scratch_peak_bytes", "cgb_scratch_reset_peak",
     "cgb_scratch_set_limit", "cgb_scratch_release", "cgb_last_error", "cgb_version",
     "cgb_kernel_launch_count", "cgb_last_path", "cgb_debug_sw_stats", "cgb_set_tuning", "cgb_get_tuning",
-    "cgb_scratch_cached_bytes",
+    "cgb_scratch_cached_bytes", "cgb_im2col_host", "cgb_gemm_host",
+    "cgb_conv_f64", "cgb_conv_host_f64", "cgb_im2col_host_f64", "cgb_gemm_host_f64",
 )
 
 
@@ -61,6 +62,12 @@ def _load() -> ctypes.CDLL:
         "cgb_scratch_set_limit": (None, [ctypes.c_uint64]),
         "cgb_scratch_release": (None, []),
         "cgb_scratch_cached_bytes": (ctypes.c_uint64, []),
+        "cgb_im2col_host": (st, [vp, cpp, vp, i64]),
+        "cgb_gemm_host": (st, [ctypes.c_int, vp, i64, vp, i64, vp, i64, i64, i64, i64, ctypes.c_int]),
+        "cgb_conv_f64": (st, [ctypes.c_int, vp, vp, cpp, bpp, vp, vp]),
+        "cgb_conv_host_f64": (st, [ctypes.c_int, vp, vp, cpp, bpp, vp]),
+        "cgb_im2col_host_f64": (st, [vp, cpp, vp, i64]),
+        "cgb_gemm_host_f64": (st, [vp, i64, vp, i64, vp, i64, i64, i64, i64, bpp, ctypes.c_int]),
         "cgb_last_error": (ctypes.c_char_p, []),
         "cgb_version": (ctypes.c_char_p, []),
         "cgb_kernel_launch_count": (ctypes.c_uint64, []),

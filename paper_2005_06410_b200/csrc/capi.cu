@@ -329,6 +329,7 @@ cgb_status cgb_validate_blocking(const cgb_blocking_params* bp) {
 int64_t cgb_conv_workspace_bytes(int algo, int precision, const cgb_conv_params* cp) {
   ConvGeom g;
   if (make_geom(cp, &g)) return -1;
+  if (algo == CGB_ALGO_DIRECT) return 0;
   const int prec = resolve_precision(precision, g);
   const Plan pl = make_plan(algo, prec, g, nullptr);
   return std::max<int64_t>(pl.f_bytes + pl.b_bytes, use_wim(algo, prec, g) ? wim_filter_bytes(prec, g) : 0);
@@ -342,6 +343,12 @@ static cgb_status conv_impl(int algo, int precision, const float* F, const float
                             int64_t ldb_ext) {
   cgb_status st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (algo == CGB_ALGO_DIRECT) {  // the reference's seven-loop convolution (no workspace)
+    const cudaError_t e = launch_direct_conv(F, I, O, g, s);
+    if (e != cudaSuccess) return cuda_fail(e, "conv_direct kernel launch");
+    g_last_path = 8;
+    return CGB_OK;
+  }
   const int prec = resolve_precision(precision, g);
   Plan pl = make_plan(algo, prec, g, F);
   if (Bext) {
@@ -436,7 +443,8 @@ cgb_status cgb_conv(int algo, int precision, const float* F, const float* I, con
   ConvGeom g;
   cgb_status st = make_geom(cp, &g);
   if (st) return st;
-  if (algo != CGB_ALGO_EXPLICIT && algo != CGB_ALGO_FUSED) return fail(CGB_INVALID_ARGUMENT, "unknown algo");
+  if (algo != CGB_ALGO_EXPLICIT && algo != CGB_ALGO_FUSED && algo != CGB_ALGO_DIRECT)
+    return fail(CGB_INVALID_ARGUMENT, "unknown algo");
   if (precision < CGB_PREC_AUTO || precision > CGB_PREC_FFMA)
     return fail(CGB_INVALID_ARGUMENT, "unknown precision");
   if (!F || !I || !O) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
@@ -564,6 +572,191 @@ cgb_status cgb_conv_host(int algo, int precision, const float* F_host, const flo
   const cudaError_t e = run_host_pipeline(io, s, &where);
   if (ctx.st != CGB_OK) return ctx.st;  // cgb_conv already set the message
   if (e != cudaSuccess) return cuda_fail(e, where.c_str());
+  return CGB_OK;
+}
+
+// ---- host-pointer im2col and gemm (the reference's other host entry points)
+namespace {
+struct DevBuf {  // device staging for one synchronous host call
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, std::max<size_t>(n, 256)); }
+};
+}  // namespace
+
+cgb_status cgb_im2col_host(const float* I_host, const cgb_conv_params* cp, float* B_host, int64_t ldb) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (!I_host || !B_host) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  if (ldb < g.k) return fail(CGB_DIMENSION_MISMATCH, "leading dimension smaller than k");
+  if ((st = check_device_limits(g))) return st;
+  const size_t ib = (size_t)(g.h_i * g.w_i * g.c_i * g.b) * 4, bb = (size_t)(ldb * g.n) * 4;
+  DevBuf dI, dB;
+  cudaError_t e;
+  if ((e = dI.alloc(ib)) != cudaSuccess || (e = dB.alloc(bb)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CGB_ALLOCATION_FAILURE, "cannot allocate device staging for im2col");
+  }
+  if ((e = cudaMemcpy(dI.p, I_host, ib, cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e, "im2col H2D");
+  if ((e = launch_im2col(static_cast<const float*>(dI.p), static_cast<float*>(dB.p), ldb, g, nullptr)) != cudaSuccess)
+    return cuda_fail(e, "im2col");
+  if ((e = cudaMemcpy(B_host, dB.p, bb, cudaMemcpyDeviceToHost)) != cudaSuccess) return cuda_fail(e, "im2col D2H");
+  return CGB_OK;
+}
+
+cgb_status cgb_gemm_host(int precision, const float* A_host, int64_t lda, const float* B_host, int64_t ldb,
+                         float* C_host, int64_t ldc, int64_t m, int64_t n, int64_t k, int accumulate) {
+  if (m < 1 || n < 1 || k < 1) return fail(CGB_INVALID_GEOMETRY, "gemm dimensions must be positive");
+  if (lda < m || ldb < k || ldc < m) return fail(CGB_DIMENSION_MISMATCH, "leading dimension smaller than rows");
+  if (!A_host || !B_host || !C_host) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  const int64_t ldbp = (k + 3) / 4 * 4;  // the device B gets a 16-byte leading dimension
+  DevBuf dA, dB, dC;
+  cudaError_t e;
+  if ((e = dA.alloc((size_t)(m * k) * 4)) != cudaSuccess || (e = dB.alloc((size_t)(ldbp * n) * 4)) != cudaSuccess ||
+      (e = dC.alloc((size_t)(m * n) * 4)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CGB_ALLOCATION_FAILURE, "cannot allocate device staging for gemm");
+  }
+  // dense copies (the device kernels take lda == ldc == m)
+  if ((e = cudaMemcpy2D(dA.p, (size_t)m * 4, A_host, (size_t)lda * 4, (size_t)m * 4, (size_t)k,
+                        cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy2D(dB.p, (size_t)ldbp * 4, B_host, (size_t)ldb * 4, (size_t)k * 4, (size_t)n,
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(e, "gemm H2D");
+  if (ldbp != k && (e = cudaMemset2D(static_cast<char*>(dB.p) + k * 4, (size_t)ldbp * 4, 0, (size_t)(ldbp - k) * 4,
+                                     (size_t)n)) != cudaSuccess)
+    return cuda_fail(e, "gemm B padding");
+  cgb_status st = cgb_gemm(precision, static_cast<const float*>(dA.p), m, static_cast<const float*>(dB.p), ldbp,
+                           static_cast<float*>(dC.p), m, m, n, k, nullptr, 0, nullptr);
+  if (st) return st;
+  std::vector<float> tmp;
+  float* dst = C_host;
+  int64_t ldd = ldc;
+  if (accumulate) {
+    tmp.resize((size_t)(m * n));
+    dst = tmp.data();
+    ldd = m;
+  }
+  if ((e = cudaMemcpy2D(dst, (size_t)ldd * 4, dC.p, (size_t)m * 4, (size_t)m * 4, (size_t)n,
+                        cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return cuda_fail(e, "gemm D2H");
+  if (accumulate)
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < m; ++i) C_host[i + j * ldc] += tmp[(size_t)(i + j * m)];
+  return CGB_OK;
+}
+
+// ---- float64: the reference's f64 instantiations on the device, bit-identical
+static int64_t kc_of(const cgb_blocking_params* bp) { return bp ? bp->kc : 640; }
+
+cgb_status cgb_conv_f64(int algo, const double* F, const double* I, const cgb_conv_params* cp,
+                        const cgb_blocking_params* bp, double* O, void* stream) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if ((st = cgb_validate_blocking(bp))) return st;
+  if (!F || !I || !O) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  if (algo != CGB_ALGO_EXPLICIT && algo != CGB_ALGO_FUSED && algo != CGB_ALGO_DIRECT)
+    return fail(CGB_INVALID_ARGUMENT, "unknown algo");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (algo == CGB_ALGO_DIRECT) {
+    e = launch_direct_conv_f64(F, I, O, g, s);
+  } else if (algo == CGB_ALGO_FUSED) {
+    e = launch_refgemm_f64(F, g.k_n, nullptr, 0, I, g, O, g.k_n, g.m, g.n, g.k, kc_of(bp), false, s);
+  } else {
+    // the reference materialises B-hat (k x n) and runs the same gemm over it
+    void* ws = nullptr;
+    const size_t need = (size_t)(g.k * g.n) * sizeof(double);
+    if ((st = scratch_get(need, &ws, s))) return st;
+    struct Release {
+      size_t n;
+      ~Release() { scratch_done(n); }
+    } release{need};
+    double* B = static_cast<double*>(ws);
+    if ((e = launch_im2col_f64(I, B, g.k, g, s)) != cudaSuccess) return cuda_fail(e, "im2col f64");
+    e = launch_refgemm_f64(F, g.k_n, B, g.k, nullptr, g, O, g.k_n, g.m, g.n, g.k, kc_of(bp), false, s);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "f64 conv kernel launch");
+  g_last_path = 9;
+  return CGB_OK;
+}
+
+cgb_status cgb_conv_host_f64(int algo, const double* F_host, const double* I_host, const cgb_conv_params* cp,
+                             const cgb_blocking_params* bp, double* O_host) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (!F_host || !I_host || !O_host) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  const size_t fb = (size_t)(g.k_n * g.k) * 8, ib = (size_t)(g.c_i * g.h_i * g.w_i * g.b) * 8,
+               ob = (size_t)(g.k_n * g.n) * 8;
+  DevBuf dF, dI, dO;
+  cudaError_t e;
+  if ((e = dF.alloc(fb)) != cudaSuccess || (e = dI.alloc(ib)) != cudaSuccess || (e = dO.alloc(ob)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CGB_ALLOCATION_FAILURE, "cannot allocate device staging for the f64 host path");
+  }
+  if ((e = cudaMemcpy(dF.p, F_host, fb, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(dI.p, I_host, ib, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(e, "f64 H2D");
+  if ((st = cgb_conv_f64(algo, static_cast<const double*>(dF.p), static_cast<const double*>(dI.p), cp, bp,
+                         static_cast<double*>(dO.p), nullptr)))
+    return st;
+  if ((e = cudaMemcpy(O_host, dO.p, ob, cudaMemcpyDeviceToHost)) != cudaSuccess) return cuda_fail(e, "f64 D2H");
+  return CGB_OK;
+}
+
+cgb_status cgb_im2col_host_f64(const double* I_host, const cgb_conv_params* cp, double* B_host, int64_t ldb) {
+  ConvGeom g;
+  cgb_status st = make_geom(cp, &g);
+  if (st) return st;
+  if (!I_host || !B_host) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  if (ldb < g.k) return fail(CGB_DIMENSION_MISMATCH, "leading dimension smaller than k");
+  const size_t ib = (size_t)(g.h_i * g.w_i * g.c_i * g.b) * 8, bb = (size_t)(ldb * g.n) * 8;
+  DevBuf dI, dB;
+  cudaError_t e;
+  if ((e = dI.alloc(ib)) != cudaSuccess || (e = dB.alloc(bb)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CGB_ALLOCATION_FAILURE, "cannot allocate device staging for im2col");
+  }
+  if ((e = cudaMemcpy(dI.p, I_host, ib, cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e, "im2col H2D");
+  if ((e = launch_im2col_f64(static_cast<const double*>(dI.p), static_cast<double*>(dB.p), ldb, g, nullptr)) !=
+      cudaSuccess)
+    return cuda_fail(e, "im2col f64");
+  if ((e = cudaMemcpy(B_host, dB.p, bb, cudaMemcpyDeviceToHost)) != cudaSuccess) return cuda_fail(e, "im2col D2H");
+  return CGB_OK;
+}
+
+cgb_status cgb_gemm_host_f64(const double* A_host, int64_t lda, const double* B_host, int64_t ldb, double* C_host,
+                             int64_t ldc, int64_t m, int64_t n, int64_t k, const cgb_blocking_params* bp,
+                             int accumulate) {
+  if (m < 1 || n < 1 || k < 1) return fail(CGB_INVALID_GEOMETRY, "gemm dimensions must be positive");
+  if (lda < m || ldb < k || ldc < m) return fail(CGB_DIMENSION_MISMATCH, "leading dimension smaller than rows");
+  if (!A_host || !B_host || !C_host) return fail(CGB_INVALID_ARGUMENT, "null tensor pointer");
+  cgb_status st = cgb_validate_blocking(bp);
+  if (st) return st;
+  DevBuf dA, dB, dC;
+  cudaError_t e;
+  if ((e = dA.alloc((size_t)(lda * k) * 8)) != cudaSuccess || (e = dB.alloc((size_t)(ldb * n) * 8)) != cudaSuccess ||
+      (e = dC.alloc((size_t)(ldc * n) * 8)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CGB_ALLOCATION_FAILURE, "cannot allocate device staging for gemm");
+  }
+  if ((e = cudaMemcpy(dA.p, A_host, (size_t)(lda * k) * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(dB.p, B_host, (size_t)(ldb * n) * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (accumulate && (e = cudaMemcpy(dC.p, C_host, (size_t)(ldc * n) * 8, cudaMemcpyHostToDevice)) != cudaSuccess))
+    return cuda_fail(e, "gemm H2D");
+  ConvGeom g{};
+  if ((e = launch_refgemm_f64(static_cast<const double*>(dA.p), lda, static_cast<const double*>(dB.p), ldb, nullptr, g,
+                              static_cast<double*>(dC.p), ldc, m, n, k, kc_of(bp), accumulate != 0, nullptr)) !=
+      cudaSuccess)
+    return cuda_fail(e, "gemm f64");
+  if ((e = cudaMemcpy2D(C_host, (size_t)ldc * 8, dC.p, (size_t)ldc * 8, (size_t)m * 8, (size_t)n,
+                        cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return cuda_fail(e, "gemm D2H");
   return CGB_OK;
 }
 

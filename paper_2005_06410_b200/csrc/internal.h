@@ -59,6 +59,16 @@ cudaError_t launch_im2col(const float* I, float* B, int64_t ldb, const ConvGeom&
 cudaError_t launch_ffma_conv(const float* F, const float* I, const float* explicit_src, int64_t ldb, float* O,
                              const ConvGeom& g, cudaStream_t st);
 
+// The reference's arithmetic bit for bit (ref_order.cu): conv_direct (conv.hpp:24-55),
+// the kc-blocked gemm order (gemm.hpp:46-97) and im2col, for float and double.
+cudaError_t launch_direct_conv(const float* F, const float* I, float* O, const ConvGeom& g, cudaStream_t st);
+cudaError_t launch_direct_conv_f64(const double* F, const double* I, double* O, const ConvGeom& g, cudaStream_t st);
+// C = A * B in the reference's kc-blocked order; B == nullptr: the lowered matrix of g from I.
+cudaError_t launch_refgemm_f64(const double* A, int64_t lda, const double* B, int64_t ldb, const double* I,
+                               const ConvGeom& g, double* C, int64_t ldc, int64_t m, int64_t n, int64_t K, int64_t kc,
+                               bool accumulate, cudaStream_t st);
+cudaError_t launch_im2col_f64(const double* I, double* B, int64_t ldb, const ConvGeom& g, cudaStream_t st);
+
 // K5: filter preparation. Writes F (k_n x K, ld = k_n) into hi (and lo when
 // lo != nullptr) with leading dimension ldf >= k_n, zero padding n >= k_n.
 // hi = tf32_rna(f), lo = tf32_rna(f - hi)  (3xTF32 split); with lo == nullptr hi = f.

@@ -66,6 +66,32 @@ def main():
         out[f"med{i}_O"] = R.conv_gemm(F, I, cp, threads=2)
         out[f"med{i}_Oexplicit"] = R.conv_im2col_gemm(F, I, cp, threads=3)
     out["n_med"] = np.array(len(medium))
+    # 3. float64 (the reference's f64 instantiations, README.md:38-40): conv_gemm /
+    #    conv_im2col_gemm / conv_direct / im2col at double precision on the acceptance
+    #    stream (seed 202), plus two shapes with K > kc (two and four kc blocks, the second
+    #    with kc = 100) and a gemm -- the device f64 path must match these bit for bit.
+    g = R.rng(202)
+    f64_cases = [g.conv_params(8, 3) for _ in range(24)]
+    f64_cases += [dict(k_n=40, k_h=3, k_w=3, c_i=96, h_i=9, w_i=9, b=2, s=1, p=1),
+                  dict(k_n=24, k_h=3, k_w=3, c_i=40, h_i=8, w_i=7, b=2, s=2, p=1)]
+    kcs = [640] * 25 + [100]
+    for i, cp in enumerate(f64_cases):
+        F = g.tensor(cp["k_n"], cp["k_h"], cp["k_w"], cp["c_i"], dtype=np.float64)
+        I = g.tensor(cp["h_i"], cp["w_i"], cp["c_i"], cp["b"], dtype=np.float64)
+        bp = (120, 3072, kcs[i], 8, 12)
+        out[f"f64_{i}_cp"] = cp_vec(cp)
+        out[f"f64_{i}_kc"] = np.array(kcs[i])
+        out[f"f64_{i}_F"] = F
+        out[f"f64_{i}_I"] = I
+        out[f"f64_{i}_O"] = R.conv_gemm(F, I, cp, threads=2, bp=bp)
+        out[f"f64_{i}_Oexplicit"] = R.conv_im2col_gemm(F, I, cp, threads=1, bp=bp)
+        out[f"f64_{i}_Odirect"] = R.conv_direct(F, I, cp)
+        out[f"f64_{i}_B"] = R.im2col(I, cp)
+    out["n_f64"] = np.array(len(f64_cases))
+    A = g.tensor(37, 700, 1, 1, dtype=np.float64).reshape(37, 700, order="F")
+    Bm = g.tensor(700, 19, 1, 1, dtype=np.float64).reshape(700, 19, order="F")
+    out["f64_gemm_A"], out["f64_gemm_B"] = A, Bm
+    out["f64_gemm_C"] = R.gemm(A, Bm, threads=2)
     path = os.path.join(HERE, "reference_conv.npz")
     np.savez_compressed(path, **out)
     print(path, os.path.getsize(path), "bytes")
