@@ -19,13 +19,15 @@ Host-side mirror of the reference's model and benchmark layer:
 
 Algorithms (bench.hpp:13-19): ``convgemm`` = fused operator, ``im2col`` = explicit
 (B-hat in HBM), ``gemm-only`` = the explicit GEMM over a B-hat lowered outside the timed
-region, ``im2col-only`` = the lowering alone (no FLOPs, no output), ``direct`` = the
-FFMA kernel (fp32 FMA accumulation, the device's stand-in for conv_direct).
-``check`` compares every conv output with the FFMA kernel's, as the reference compares
-with conv_direct (bench.cpp:227-233), under the north star's per-output normalisation
-|O - O_ffma| / (||F[i_k]|| * ||B-hat[:, col]||) <= 1e-5 (5e-3 in plain TF32 mode). (The
-reference's own max(1, max|ref|) normalisation is too strict for any two fp32
-summation orders once K is in the thousands.)
+region, ``im2col-only`` = the lowering alone (no FLOPs, no output), ``direct`` =
+conv_direct on the device, bit-identical to the reference's conv_direct<float>
+(ref_order.cu). ``check`` compares every conv output with conv_direct, as the reference
+does (bench.cpp:212-233), under the north star's per-output bar |O - O_direct| /
+(||F[i_k]|| * ||B-hat[:, col]||) <= 1e-5 for the fp32-accurate precisions (5e-3 in plain
+TF32 mode). The reference's own max|O - O_direct| / max(1, max|O_direct|) <= 1e-5 is a
+bar for two IEEE fp32 summation orders; the tensor cores' fp32 accumulation is not
+IEEE round-to-nearest, and on the simulator's growing activations 3xTF32 lands at
+~1.1e-5 on it (ResNet-50 layer 14 at b=2) while meeting the per-output bar by 10x.
 """
 from __future__ import annotations
 
@@ -234,7 +236,7 @@ def run_inference(model: ModelSpec, batch: int, algo: str = "convgemm", threads:
         if layer.kind == "fc":
             m, n, k = layer.fc_m, batch, layer.fc_k
             W, X, Y = _view2(weights, m, k), _view2(src, k, n), _view2(dst, m, n)
-            prec = "ffma" if algo == "direct" else precision
+            prec = precision  # fc layers are gemm under every algo (bench.cpp:140-153)
             op = lambda W=W, X=X, Y=Y, prec=prec: gemm(W, X, precision=prec, out=Y)  # noqa: E731
             ws = conv_workspace_bytes(_fc_params(layer, batch), "explicit", prec, external_b=True)
         else:
@@ -244,10 +246,12 @@ def run_inference(model: ModelSpec, batch: int, algo: str = "convgemm", threads:
             F = _view4(weights, cp.k_n, cp.k_h, cp.k_w, cp.c_i)
             I = _view4(src, cp.h_i, cp.w_i, cp.c_i, batch)
             O = _view4(dst, cp.k_n, h_o, w_o, batch)
-            if algo in ("convgemm", "direct"):
-                prec = "ffma" if algo == "direct" else precision
-                op = lambda F=F, I=I, O=O, cp=cp, prec=prec: conv(F, I, cp, "fused", prec, out=O)  # noqa: E731
-                ws = conv_workspace_bytes(cp, "fused", prec)
+            if algo == "convgemm":
+                op = lambda F=F, I=I, O=O, cp=cp: conv(F, I, cp, "fused", precision, out=O)  # noqa: E731
+                ws = conv_workspace_bytes(cp, "fused", precision)
+            elif algo == "direct":
+                op = lambda F=F, I=I, O=O, cp=cp: conv(F, I, cp, "direct", out=O)  # noqa: E731
+                ws = 0
             elif algo == "im2col":
                 op = lambda F=F, I=I, O=O, cp=cp: conv(F, I, cp, "explicit", precision, out=O)  # noqa: E731
                 ws = conv_workspace_bytes(cp, "explicit", precision)
@@ -279,8 +283,9 @@ def run_inference(model: ModelSpec, batch: int, algo: str = "convgemm", threads:
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) * 1e-3 / reps
         if check and layer.kind == "conv" and wrote and algo != "direct":
-            err = _check_error(conv, F, I, O, cp)
-            tol = 5e-3 if precision == "tf32" else 1e-5
+            ref = torch.empty_like(O)
+            conv(F, I, cp, "direct", out=ref)  # the reference's checker, bit-identical
+            err, tol = _per_output_error(conv, F, I, O, ref, cp), (5e-3 if precision == "tf32" else 1e-5)
             if err > tol:
                 raise RuntimeError(f"check failed at layer {li}: error {err:g}")
         results.append(LayerResult(li, layer.kind, m, n, k, t, reps, flops / t / 1e9 if flops else 0.0, ws))
@@ -289,15 +294,13 @@ def run_inference(model: ModelSpec, batch: int, algo: str = "convgemm", threads:
     return results
 
 
-def _check_error(conv, F, I, O, cp):
-    """max over outputs of |O - O_ffma| / (||F[i_k]|| * ||B-hat[:, col]||): the north
-    star's per-output normalisation, against the FFMA kernel. The column norms of the
-    lowered matrix come from one more convolution: ones-filters over I*I."""
+def _per_output_error(conv, F, I, O, ref, cp):
+    """max over outputs of |O - O_ref| / (||F[i_k]|| * ||B-hat[:, col]||): the north
+    star's per-output normalisation. The column norms of the lowered matrix come from one
+    more convolution: ones-filters over I*I."""
     import torch
 
     from . import ConvParams
-    ref = torch.empty_like(O)
-    conv(F, I, cp, "fused", "ffma", out=ref)
     fn = F.pow(2).sum(dim=(1, 2, 3)).sqrt()  # (k_n,)
     c4 = ConvParams(4, cp.k_h, cp.k_w, cp.c_i, cp.h_i, cp.w_i, cp.b, cp.s, cp.p)
     ones = torch.ones((cp.c_i, cp.k_w, cp.k_h, 4), device=F.device).permute(3, 2, 1, 0)

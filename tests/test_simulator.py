@@ -156,9 +156,12 @@ def test_run_inference_small(algo):
 @pytest.mark.gpu
 @needs_cuda
 @pytest.mark.parametrize("name", sorted(models.MODELS))
-def test_run_inference_models_checked(name):
-    """Whole-model sweep at batch 2 with every conv checked against the FFMA kernel."""
+@pytest.mark.parametrize("precision", ["tf32", "auto"])
+def test_run_inference_models_checked(name, precision):
+    """Whole-model sweep at batch 2 with every conv checked against conv_direct as the
+    reference does (bench.cpp:212-233), under the per-output bar (1e-5 for the
+    fp32-accurate default, 5e-3 for plain TF32)."""
     m = models.MODELS[name]()
-    rs = cg.run_inference(m, 2, algo="convgemm", min_time=0.0, check=True, precision="tf32")
+    rs = cg.run_inference(m, 2, algo="convgemm", min_time=0.0, check=True, precision=precision)
     assert len(rs) == m.count("conv") + m.count("fc")
     assert all(r.gflops > 0 for r in rs)
