@@ -259,9 +259,12 @@ static bool tf32_family(int prec) { return prec == CGB_PREC_TF32 || prec == CGB_
 
 static int resolve_precision(int prec, const ConvGeom& g) {
   if (prec != CGB_PREC_AUTO) return prec;
-  // fp32-accurate choice: FFMA where the contraction is too short to feed the tensor
-  // cores (K < 32, e.g. VGG conv1 with K = 27), 3xTF32 otherwise.
-  return g.k < 32 ? CGB_PREC_FFMA : CGB_PREC_3XTF32;
+  // fp32-accurate choice by measured cost: 3xTF32 on the tensor cores wherever a
+  // shifted-window kernel takes the layer -- including the low-channel w-im2col rows
+  // (VGG conv1, K = 27: 323 us vs 508 us for FFMA at b=64, profiles/r01_configs.json);
+  // FFMA only for short contractions no tensor-core layout covers.
+  if (g.k < 32 && !shifted_supported(g) && !wim_supported(g)) return CGB_PREC_FFMA;
+  return CGB_PREC_3XTF32;
 }
 
 static bool use_wim(int algo, int prec, const ConvGeom& g) {
