@@ -72,12 +72,14 @@ template <bool EXPLICIT>
 CGB_DEV void gather_chunk(const Args& a, const RowState& rs, const ChunkState& cs, const float* Bexp, int64_t P,
                           float (&v)[4]) {
   if (EXPLICIT) {
-    if (rs.ok && cs.r + 3 < a.ldb) {
+    // rows >= K of a caller's B (ldb > k, gemm.hpp) are not part of the operand: bounded
+    // by K, not ldb (they would otherwise meet zero filter rows, and 0 * NaN/Inf = NaN)
+    if (rs.ok && cs.r + 3 < a.K) {
       const float4 x = __ldg(reinterpret_cast<const float4*>(Bexp + P * a.ldb + cs.r));
       v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
     } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = (rs.ok && cs.r + e < a.ldb) ? __ldg(Bexp + P * a.ldb + cs.r + e) : 0.0f;
+      for (int e = 0; e < 4; ++e) v[e] = (rs.ok && cs.r + e < a.K) ? __ldg(Bexp + P * a.ldb + cs.r + e) : 0.0f;
     }
   } else {
     int32_t c = cs.c, kw = cs.kw, kh = cs.kh;

@@ -165,3 +165,26 @@ def test_run_inference_models_checked(name, precision):
     rs = cg.run_inference(m, 2, algo="convgemm", min_time=0.0, check=True, precision=precision)
     assert len(rs) == m.count("conv") + m.count("fc")
     assert all(r.gflops > 0 for r in rs)
+
+
+@pytest.mark.gpu
+def test_gemm_ignores_rows_past_k():
+    """B with ldb > k (a view of a taller matrix): rows k..ldb-1 are not part of the
+    operand, even when they hold NaN/Inf (the explicit gather was bounded by
+    ldb)."""
+    import numpy as np
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    rng = np.random.default_rng(5)
+    m, n, k, ldb = 96, 40, 52, 64
+    A = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    Bfull = rng.uniform(-1, 1, (ldb, n)).astype(np.float32)
+    Bfull[k:, :] = np.nan
+    Ad = torch.from_numpy(np.ascontiguousarray(A.T)).cuda().t()
+    Bd = torch.from_numpy(np.ascontiguousarray(Bfull.T)).cuda().t()[:k]  # (k, n) view, ld = 64
+    for prec in ("tf32", "3xtf32", "ffma"):
+        C = cg.gemm(Ad, Bd, precision=prec).cpu().numpy()
+        ref = A.astype(np.float64) @ Bfull[:k].astype(np.float64)
+        assert np.isfinite(C).all(), prec
+        assert np.abs(C - ref).max() <= (5e-3 if prec == "tf32" else 1e-5) * np.abs(A).sum(1).max(), prec
