@@ -165,7 +165,7 @@ uint64_t cgb_scratch_cached_bytes(void);
  * Keys: "sk" (stream-K: 0 never, 1 auto, 2 always), "tail" (tail tiles: 0/1/2), "pair"
  * (CTA pairs allowed), "cfg" (force a kernel candidate, -1 auto), "mt", "bn" (force
  * tile sizes, 0 auto), "tma_a", "tma_deep" (1x1-layer variants), "pstore", "pdl",
- * "verbose", "smem_pad_kb", "tps", "host_chunk_kb", "host_no_bounce", "host_copy_threads",
+ * "verbose", "smem_pad_kb", "tps", "splitk", "host_chunk_kb", "host_no_bounce", "host_copy_threads",
  * "debug" (profiling builds only). Every setting gives a correct result; unknown keys
  * return CGB_INVALID_ARGUMENT. The library reads no environment variables. */
 cgb_status cgb_set_tuning(const char* key, int64_t value);

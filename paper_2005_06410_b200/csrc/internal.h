@@ -31,6 +31,7 @@ struct Tuning {
   int verbose = 0;       // print the chosen configuration to stderr
   int smem_pad_kb = 0;   // pad dynamic shared memory (shrinks the L1 carve-out)
   int tps = 0;           // shifted-window filter taps per stage hand-over (0 = by cost)
+  int splitk = 0;        // split-K pieces for few-tile layers: -1 never, 0 auto, S forced
   int64_t host_chunk_kb = 8192;  // host path: chunk size of the H2D || conv || D2H pipeline
   int host_no_bounce = 0;        // host path: DMA pageable buffers directly (no pinned ring)
   int host_copy_threads = 0;     // host path: memcpy pool size (0 = min(8, cores/2))

@@ -83,6 +83,12 @@ struct Args {
   int* counters;      // [sk tile][ranks*4 epilogue warps][2] pieces arrived / written; zero between launches
   float* sk_ws;       // partial tiles of split pieces: [sk tile][rank][sk_pieces][MT*128 x BN]
   int32_t sk_pieces;  // most pieces any split tile has
+  // Split-K (layers with fewer tiles than half the groups, e.g. 7x7 512->512 at b=16):
+  // the stream-K split of every tile into S equal pieces (S divides CC, groups = tiles*S,
+  // one piece per group); each piece writes its partial tile to sk_ws slot (tile, rank,
+  // piece) and splitk_reduce_kernel sums the S slots in order into O. No CTA waits for
+  // another. 0/1 = off.
+  int32_t splitk;
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
   int32_t tps;        // taps per filter stage group (divides B_STAGES; see the filter TMA warp)
@@ -268,14 +274,14 @@ CGB_DEV void issue_tap_partial(uint32_t d_base, uint64_t at, uint64_t at_lo, uin
 // Epilogue of one accumulator set: TMEM -> registers -> O for the units u = u0, u0 + du,
 // ... of the tile's (M subtile, 32-column block) pairs, for the 32 rows of TMEM lane
 // quadrant `sub` (the calling warp's warp % 4).
-// Stream-K pieces (sk_mode): 1 = write this piece's partial to its workspace slot
-// (ws_own: [unit][sub][lane][32] floats, each lane one 128-byte run), 2 = the last piece
-// to arrive: O = p_0 + p_1 + ... in piece order (own registers at position prank, the
-// others from the workspace slots ws_all + r * piece_stride), then store as usual;
-// 3 = red.add into O (the second of two pieces).
-template <int BN>
+// MODE 0: store into O (add: red.add instead -- the second of two stream-K pieces);
+// 1: write this piece's partial to its workspace slot (ws_own: [unit][sub][lane][32]
+// floats, each lane one 128-byte run); 2: the last piece to arrive: O = p_0 + p_1 + ...
+// in piece order (own registers at position prank, the others from the workspace slots
+// ws_all + r * piece_stride), then store. Compile-time modes keep the common loop lean.
+template <int BN, int MODE>
 CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, int32_t m0, int n0, int mtc, int sub,
-                         int lane, int u0, int du, int sk_mode = 0, float* ws_own = nullptr,
+                         int lane, int u0, int du, bool add = false, float* ws_own = nullptr,
                          const float* ws_all = nullptr, size_t piece_stride = 0, int npieces = 1, int prank = 0) {
   constexpr int NCB = BN / 32;
   const int32_t hw_q = a.Hq * a.Wq;
@@ -295,12 +301,12 @@ CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, i
     tmem_ld_32x32b_x32(trow + cb * 32, r);
     tmem_ld_wait();
     const size_t run = ((size_t)(u * 4 + sub) * 32 + lane) * 32;  // this lane's 32 floats in a piece slot
-    if (sk_mode == 1) {
+    if (MODE == 1) {
 #pragma unroll
       for (int j = 0; j < 32; j += 8) st_global_v8(ws_own + run + j, &r[j]);
       continue;
     }
-    if (sk_mode == 2) {
+    if (MODE == 2) {
       // four columns at a time (registers: the kernel runs at its launch bound)
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
@@ -322,7 +328,6 @@ CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, i
         for (int i = 0; i < 4; ++i) r[j + i] = __float_as_uint(acc[i]);
       }
     }
-    const bool add = sk_mode == 3;
     const int nb = n0 + cb * 32;
     if (a.pstore && a.vec && nb + 32 <= a.k_n && !CGB_DBG(4)) {
       // Lane pairs write whole 64-byte runs: in store A_k the pair writes segments
@@ -378,6 +383,60 @@ CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, i
             else atomicAdd(dst + j, __uint_as_float(r[j]));
           }
       }
+    }
+  }
+}
+
+// Split-K: O = slot_0 + slot_1 + ... + slot_{S-1} for every output of every tile (the
+// fixed order makes the result independent of which piece finished first). Slot layout
+// per (tile, CTA rank): [unit = (subtile, 32-column block)][TMEM quadrant][lane][32],
+// as store_units writes it; one thread per 4 consecutive columns of one row.
+template <int MT, int BN, bool PAIR>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(float* __restrict__ O, Args a) {
+  griddep_wait();  // the partial tiles of the previous grid (launched with PDL)
+  constexpr int NCB = BN / 32, P = PAIR ? 2 : 1;
+  const int64_t piece = (int64_t)MT * 128 * BN;
+  const int64_t per_tile = (int64_t)P * piece / 4;  // float4 items per tile (both ranks)
+  const int64_t total = (int64_t)a.m_tiles * a.n_tiles * per_tile;
+  const int32_t hw_q = a.Hq * a.Wq;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int tile = (int)(idx / per_tile);
+    int64_t r = idx - (int64_t)tile * per_tile;
+    const int rank = (int)(r / (piece / 4));
+    r -= (int64_t)rank * (piece / 4);
+    const int j4 = (int)(r & 7);  // float4 within the lane's 32-float run
+    const int64_t run = r >> 3;   // (unit, sub, lane)
+    const int lane = (int)(run & 31), sub = (int)((run >> 5) & 3), u = (int)(run >> 7);
+    const int mt = u / NCB, cb = u - mt * NCB;
+    int32_t m0;
+    int mtc;
+    tile_rows<MT, PAIR>(a, tile, (uint32_t)rank, m0, mtc);
+    if (mt >= mtc) continue;
+    const int32_t Q = m0 + mt * 128 + sub * 32 + lane;
+    if (Q >= a.Mp32) continue;
+    const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
+    const int32_t rem = Q - bb * hw_q;
+    const int32_t wq = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wq * a.Hq;
+    if (hq >= a.h_o || wq >= a.w_o) continue;
+    const int64_t Pix = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
+    const int col = (tile / a.m_tiles) * BN + cb * 32 + 4 * j4;
+    const float* src = a.sk_ws + ((int64_t)tile * P + rank) * a.splitk * piece + run * 32 + 4 * j4;
+    float4 acc = *reinterpret_cast<const float4*>(src);
+    for (int sp = 1; sp < a.splitk; ++sp) {
+      const float4 v = *reinterpret_cast<const float4*>(src + sp * piece);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    float* dst = O + Pix * a.k_n + col;
+    if (a.vec && col + 4 <= a.k_n) {
+      *reinterpret_cast<float4*>(dst) = acc;
+    } else {
+      const float v4[4] = {acc.x, acc.y, acc.z, acc.w};
+      for (int e = 0; e < 4; ++e)
+        if (col + e < a.k_n) dst[e] = v4[e];
     }
   }
 }
@@ -888,18 +947,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       // The last piece resets the counters for the next launch.
       const bool whole = cc0 == 0 && cc1 == a.CC;
       const uint32_t trow0 = tmem_base + ((uint32_t)(sub * 32) << 16) + acc_set * C::ACC_COLS;
+      // one call site per store mode plus a dedicated one for whole tiles (constant
+      // folding keeps the common loop free of the red.add branch); an out-of-line call
+      // measured far slower: the call ABI reshapes the whole kernel's register allocation
+      bool add = false;  // plain stores, or red.adds for the second of two stream-K pieces
+      int mode = 0;
+      float* ws_own = nullptr;
+      const float* ws_all = nullptr;
+      int* cnt = nullptr;
+      int npieces = 1, prank = 0;
+      bool last = true;
+      const size_t piece = (size_t)MT * 128 * BN;
       if (whole) {
-        store_units<BN>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1);
+        mode = 0;
       } else {
         const int u0 = tile * a.CC;  // stream-K tiles are tiles [0, sk_tiles)
         const int g_hi = sk_group_of(a, u0 + a.CC - 1);
-        const int prank = g_hi - gid;
-        const int npieces = g_hi - sk_group_of(a, u0) + 1;
-        int* cnt = a.counters + 2 * ((size_t)tile * (PAIR ? 8 : 4) + rank * 4 + sub);
+        prank = g_hi - gid;
+        npieces = g_hi - sk_group_of(a, u0) + 1;
+      }
+      if (!whole && a.splitk > 1) {  // split-K partial -> its workspace slot (splitk_reduce_kernel)
+        ws_own = a.sk_ws + (((size_t)tile * (PAIR ? 2 : 1) + rank) * a.splitk + prank) * piece;
+        mode = 1;
+      } else if (!whole) {
+        cnt = a.counters + 2 * ((size_t)tile * (PAIR ? 8 : 4) + rank * 4 + sub);
         int order = 0;
         if (lane == 0) order = atomicAdd(cnt, 1);
         order = __shfl_sync(0xffffffffu, order, 0);
-        const bool last = order + 1 == npieces;
+        last = order + 1 == npieces;
         if (last && lane == 0) {
           while (ld_acquire_gpu(cnt + 1) < npieces - 1) {  // pieces that arrived earlier
           }
@@ -911,18 +986,22 @@ __global__ void __launch_bounds__(THREADS, 1)
           __threadfence();
         }
         if (npieces == 2) {
-          store_units<BN>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, last ? 3 : 0);
+          add = last;
         } else {
-          const size_t piece = (size_t)MT * 128 * BN;
-          float* ws_all = a.sk_ws + ((size_t)tile * (PAIR ? 2 : 1) + rank) * a.sk_pieces * piece;
-          if (!last) store_units<BN>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, 1, ws_all + prank * piece);
-          else store_units<BN>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, 2, nullptr, ws_all, piece, npieces, prank);
+          float* slots = a.sk_ws + ((size_t)tile * (PAIR ? 2 : 1) + rank) * a.sk_pieces * piece;
+          ws_own = slots + prank * piece;
+          ws_all = slots;
+          mode = last ? 2 : 1;
         }
-        if (!last) {
-          __threadfence();  // the rows (O or workspace) before the "written" count
-          __syncwarp();
-          if (lane == 0) atomicAdd(cnt + 1, 1);
-        }
+      }
+      if (whole) store_units<BN, 0>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, false);  // the common path
+      else if (mode == 0) store_units<BN, 0>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, add);
+      else if (mode == 1) store_units<BN, 1>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, false, ws_own);
+      else store_units<BN, 2>(a, O, trow0, m0, n0, mtc, sub, lane, 0, 1, false, nullptr, ws_all, piece, npieces, prank);
+      if (!whole && a.splitk <= 1 && !last) {
+        __threadfence();  // the rows (O or workspace) before the "written" count
+        __syncwarp();
+        if (lane == 0) atomicAdd(cnt + 1, 1);
       }
       tc_fence_before();
       __syncwarp();
@@ -1085,6 +1164,28 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   a.counters = nullptr;
   a.sk_ws = nullptr;
   a.sk_pieces = 1;
+  a.splitk = 0;
+  // Split-K when the tiles fill less than half the groups (small batches, e.g. the 7x7
+  // and 14x14 layers of a b=16 shard): S pieces of >= 1 channel chunk per tile, partials
+  // summed in order by splitk_reduce_kernel (tuning splitk: -1 off, 0 auto, S forced).
+  {
+    int S = 0;
+    if (tu.splitk > 0) S = std::min(tu.splitk, a.CC);
+    else if (tu.splitk == 0 && 2 * tiles <= gmax) S = std::min(a.CC, gmax / std::max(tiles, 1));
+    while (S >= 2 && a.CC % S != 0) --S;  // equal pieces: one segment per group
+    if (S >= 2 && !a.tail_mt && tiles * S <= gmax) {
+      const size_t ws_bytes = (size_t)S * tiles * (PAIR ? 2 : 1) * MT * 128 * BN * sizeof(float);
+      int* cnt = nullptr;
+      float* ws = nullptr;
+      if (sk_buffers(st, 0, ws_bytes, &cnt, &ws)) {
+        a.splitk = S;
+        a.sk_ws = ws;
+        a.groups = tiles * S;
+        a.dp_tiles = 0;
+        a.sk_units = tiles * a.CC;  // the stream-K range split, one piece per group
+      }
+    }
+  }
   const int rounds = (tiles + gmax - 1) / gmax;
   const double fill = (double)tiles / ((double)rounds * gmax);
   const int sk_mode = tu.sk;
@@ -1093,7 +1194,7 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   // than the idle SMs it saves when ALL tiles would be split (1-round layers: 7x7,
   // 14x14). The fixup itself handles any number of pieces per tile (sk_mode 2 forces it).
   const bool sk_ok = !a.tail_mt && (sk_mode == 2 ? (int64_t)tiles * a.CC >= 2 * gmax : tiles >= gmax);
-  if (sk_mode != 0 && a.CC >= 2 && sk_ok && (fill < kSkFill || sk_mode == 2)) {
+  if (!a.splitk && sk_mode != 0 && a.CC >= 2 && sk_ok && (fill < kSkFill || sk_mode == 2)) {
     const int dp = std::max(0, tiles / gmax - 1) * gmax;
     const int sk_tiles = tiles - dp;
     const int units = sk_tiles * a.CC;
@@ -1122,9 +1223,9 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   if (tu.verbose)
     fprintf(stderr,
             "[cgb] launch MT=%d BN=%d split=%d A=%d B=%d pair=%d upi=%d tps=%d smem=%.1fKB tiles=%d (tail %d of mt "
-            "%d) sk_units=%d\n",
+            "%d) sk_units=%d splitk=%d\n",
             MT, BN, (int)SPLIT, A_SLOTS, B_STAGES, (int)PAIR, UPI, a.tps, smem / 1024.0, tiles,
-            a.tail_mt ? a.m_tiles - a.m_full : 0, a.tail_mt, a.sk_units);
+            a.tail_mt ? a.m_tiles - a.m_full : 0, a.tail_mt, a.sk_units, a.splitk);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((PAIR ? 2 : 1) * a.groups));
   cfg.blockDim = dim3(THREADS);
@@ -1149,6 +1250,20 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   e = cudaLaunchKernelEx(&cfg, kern, th, tl, I, O, a, a_slot_bytes);
   if (e != cudaSuccess) return e;
   count_launch();
+  if (a.splitk > 1) {  // the ordered sum of the partial tiles (PDL: waits for the grid above)
+    const int64_t items = (int64_t)tiles * (PAIR ? 2 : 1) * MT * 128 * BN / 4;
+    cudaLaunchConfig_t rc = {};
+    rc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)sms * 8)));
+    rc.blockDim = dim3(256);
+    rc.stream = st;
+    cudaLaunchAttribute ra[1];
+    ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    ra[0].val.programmaticStreamSerializationAllowed = 1;
+    rc.attrs = ra;
+    rc.numAttrs = tu.pdl ? 1 : 0;
+    if ((e = cudaLaunchKernelEx(&rc, splitk_reduce_kernel<MT, BN, PAIR>, O, a)) != cudaSuccess) return e;
+    count_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -149,11 +149,13 @@ def test_full_size_properties():
         O1 = cg.conv(F, I, cp, precision=prec)
         O2 = cg.conv(F, I, cp, precision=prec)
         assert torch.equal(O1, O2)
-        # image 37 alone
+        # image 37 alone (whole tiles, as in the b=128 launch: a split-K b=1 launch sums
+        # in another order)
         cp1 = dict(cp, b=1)
         I37 = cg.empty_tensor4(56, 56, 64, 1)
         I37.copy_(I[..., 37:38])
-        O37 = cg.conv(F, I37, cp1, precision=prec)
+        with cg.tuning(splitk=-1):
+            O37 = cg.conv(F, I37, cp1, precision=prec)
         assert torch.equal(O37[..., 0], O1[..., 37])
     # linearity (within tolerance): conv(F, 2*I) == 2*conv(F, I) exactly (power-of-two scaling)
     I2 = cg.empty_tensor4(56, 56, 64, 128)
@@ -363,13 +365,13 @@ def test_stream_k(orc, case, prec):
     ref = orc.conv_gemm(F, I, cp)
     scale = orc.output_scale(F, I, cp)
     dF, dI = to_dev(F), to_dev(I)
-    with cg.tuning(sk=sk):
+    with cg.tuning(sk=sk, splitk=-1):  # stream-K itself, not the split-K of few-tile layers
         a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
         assert cg.last_path() in ("tcgen05-shifted", "tcgen05-gather"), cg.last_path()
         b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
     assert np.array_equal(a, b), "stream-K result must not depend on which piece finishes first"
     assert per_output_error(a, ref, scale) <= TOL[prec]
-    with cg.tuning(sk=0):
+    with cg.tuning(sk=0, splitk=-1):
         whole = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
     assert per_output_error(whole, ref, scale) <= TOL[prec]
     if cg.last_path() == "tcgen05-shifted":
@@ -395,10 +397,10 @@ def test_tail_tiles(orc, case, prec):
     ref = orc.conv_gemm(F, I, cp)
     scale = orc.output_scale(F, I, cp)
     dF, dI = to_dev(F), to_dev(I)
-    with cg.tuning(tail=2):
+    with cg.tuning(tail=2, splitk=-1):
         a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
     assert per_output_error(a, ref, scale) <= TOL[prec]
-    with cg.tuning(tail=0):
+    with cg.tuning(tail=0, splitk=-1):
         b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
     assert per_output_error(b, ref, scale) <= TOL[prec]
     if cg.last_path() == "tcgen05-shifted":
@@ -581,3 +583,36 @@ def test_host_pipeline_pageable_stress():
                 scale = np.abs(dev).max()
                 assert np.max(np.abs(out - dev)) <= 1e-5 * scale
             assert np.array_equal(out, first)
+
+
+# ---------------------------------------------------------------- split-K (few-tile layers)
+SPLITK_CASES = [
+    # the strong-scaling shards of the bench layers (b=16 of 128): few tiles, many chunks
+    dict(k_n=512, k_h=3, k_w=3, c_i=512, h_i=7, w_i=7, b=16, s=1, p=1),
+    dict(k_n=512, k_h=3, k_w=3, c_i=512, h_i=14, w_i=14, b=16, s=2, p=1),
+    dict(k_n=256, k_h=3, k_w=3, c_i=256, h_i=14, w_i=14, b=4, s=1, p=1),
+    dict(k_n=96, k_h=3, k_w=3, c_i=80, h_i=9, w_i=9, b=3, s=1, p=1),
+    dict(k_n=64, k_h=1, k_w=1, c_i=256, h_i=7, w_i=7, b=2, s=1, p=0),
+]
+
+
+@pytest.mark.parametrize("case", range(len(SPLITK_CASES)))
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_split_k(orc, case, prec):
+    """Split-K partial tiles summed in a fixed order by the reduce kernel: within
+    tolerance of the oracle for every forced piece count, bitwise reproducible, and the
+    automatic choice engages for the few-tile shapes."""
+    cp = SPLITK_CASES[case]
+    F, I = rand_inputs(cp, 700 + case)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    dF, dI = to_dev(F), to_dev(I)
+    with cg.tuning(splitk=-1):
+        whole = to_host(cg.conv(dF, dI, cp, precision=prec))
+    assert per_output_error(whole, ref, scale) <= TOL[prec]
+    for S in (0, 2, 3, 5):
+        with cg.tuning(splitk=S):
+            a = to_host(cg.conv(dF, dI, cp, precision=prec))
+            b = to_host(cg.conv(dF, dI, cp, precision=prec))
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), S
+        assert per_output_error(a, ref, scale) <= TOL[prec], (S, per_output_error(a, ref, scale))
