@@ -28,7 +28,10 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--precision", default="tf32")
 ap.add_argument("--batch", type=int, default=0, help="override the stated batch")
 ap.add_argument("--graph", action="store_true", help="time the whole list as one graph replay per variant")
+ap.add_argument("--verbose", action="store_true", help="print each launch's configuration (stderr)")
 a = ap.parse_args()
+if a.verbose:
+    cg.set_tuning("verbose", 1)
 
 by_name = {l[0]: (cfg, l, cp, dist) for cfg, l, cp, dist in configs.all_layers()}
 names = [l[0] for l in configs.C2] if a.layers == "bench" else a.layers.split(",")
