@@ -1,0 +1,53 @@
+"""One launch of a non-headline kernel for ncu (profiles/r02_*): python tools/ncu_cases.py CASE
+  explicit  56x56 64->64 b=128 through the explicit path: K1 im2col_kernel + K2 tc_conv_kernel
+  ffma      VGG conv1 (224^2 3->64) b=64 on the FFMA kernel (K4)
+  fc6       VGG fc6 (4096 x 25088) at b=64 through cgb_gemm (TF32)
+  stem      the 7x7/s2 stem at b=256 (w-im2col mode of the shifted-window kernel)
+  pw56      1x1 56^2 64->256 at b=256 (TMA-fed A)
+  direct    conv_direct (bit-exact reference order) on a small layer
+Runs the operation twice (the first launch warms allocations); profile with -s/-c."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2005_06410_b200 as cg  # noqa: E402
+from paper_2005_06410_b200 import configs  # noqa: E402
+
+case = sys.argv[1]
+by = {l[0]: (c, l, cp, d) for c, l, cp, d in configs.all_layers()}
+
+
+def layer(name, b=None, **kw):
+    c, l, cp, d = by[name]
+    if b:
+        cp = dict(cp, b=b)
+    F, I = configs.make_tensors(torch, cg.empty_tensor4, cp, d, 7)
+    return cp, F, I
+
+
+for _ in range(2):
+    if case == "explicit":
+        cp, F, I = layer("r50_3x3_56_64")
+        cg.conv(F, I, cp, algo="explicit", precision="tf32")
+    elif case == "ffma":
+        cp, F, I = layer("vgg_224_3_64")
+        cg.conv(F, I, cp, precision="ffma")
+    elif case == "fc6":
+        g = torch.Generator(device="cuda").manual_seed(3)
+        A = (torch.rand((25088, 4096), generator=g, device="cuda") * 2 - 1).t()  # 4096 x 25088, column-major
+        B = (torch.rand((64, 25088), generator=g, device="cuda") * 2 - 1).t()    # 25088 x 64
+        cg.gemm(A, B, precision="tf32")
+    elif case == "stem":
+        cp, F, I = layer("stem_7x7_s2_224")
+        cg.conv(F, I, cp, precision="tf32")
+    elif case == "pw56":
+        cp, F, I = layer("pw_56_64_256")
+        cg.conv(F, I, cp, precision="tf32")
+    elif case == "direct":
+        cp, F, I = layer("r50_3x3_14_256", b=2)
+        cg.conv(F, I, cp, algo="direct")
+    torch.cuda.synchronize()
+print(case, "ok", cg.last_path())
