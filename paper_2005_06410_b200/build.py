@@ -53,8 +53,16 @@ def build(force: bool = False, verbose: bool = False, profiling: bool = False) -
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in FLAGS if f != "-shared"]
 
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
+    hdrs.append(os.path.join(os.path.dirname(HERE), "include", "convgemm_b200.h"))
+    hdrs.append(os.path.abspath(__file__))
+
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        # objects are reused while newer than their source and every header
+        if not force and os.path.exists(obj) and all(
+                os.path.getmtime(d) < os.path.getmtime(obj) for d in [src, *hdrs] if os.path.exists(d)):
+            return obj
         cmd = [NVCC, *compile_flags, *extra, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -57,7 +57,7 @@ static std::mutex g_tune_mu;
 static Tuning g_tune;
 
 #define CGB_TUNING_KEYS(X)                                                                                   \
-  X(sk) X(tail) X(pair) X(cfg) X(mt) X(bn) X(tma_a) X(tma_deep) X(pstore) X(pdl) X(verbose) X(smem_pad_kb) X(tps) X(splitk) \
+  X(sk) X(tail) X(pair) X(cfg) X(mt) X(bn) X(tma_a) X(tma_deep) X(pstore) X(pdl) X(verbose) X(smem_pad_kb) X(tps) X(splitk) X(k2_flo) \
   X(host_chunk_kb) X(host_no_bounce) X(host_copy_threads) X(debug)
 
 Tuning tuning() {
@@ -75,7 +75,7 @@ Tuning tuning() {
   env("CGB_SW_PSTORE", t.pstore); env("CGB_PDL", t.pdl); env("CGB_SW_VERBOSE", t.verbose);
   env("CGB_SW_SMEM_PAD", t.smem_pad_kb); env("CGB_HOST_CHUNK_KB", t.host_chunk_kb);
   env("CGB_HOST_NO_BOUNCE", t.host_no_bounce); env("CGB_HOST_COPY_THREADS", t.host_copy_threads);
-  env("CGB_DEBUG_SW", t.debug); env("CGB_SW_TPS", t.tps); env("CGB_SW_SPLITK", t.splitk);
+  env("CGB_DEBUG_SW", t.debug); env("CGB_SW_TPS", t.tps); env("CGB_SW_SPLITK", t.splitk); env("CGB_K2_FLO", t.k2_flo);
 #endif
   return t;
 }
@@ -142,6 +142,19 @@ cudaError_t make_filter_tmap(CUtensorMap* tm, const float* f, int64_t k_n, int64
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(f), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t make_bhat_tmap(CUtensorMap* tm, const float* b, int64_t K, int64_t n, int64_t ldb) {
+  auto enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldb * 4)};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(b), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -279,7 +292,13 @@ static Plan make_plan(int algo, int prec, const ConvGeom& g, const float* F) {
   pl.algo = algo;
   pl.prec = prec;
   pl.ldf = align_up(g.k_n, 4);
-  pl.direct_filters = prec == CGB_PREC_TF32 && g.k_n % 4 == 0 &&
+  // TF32 reads F itself through TMA. So does the explicit 3xTF32 path when the K2 kernel
+  // splits the filter lo tile in shared memory (k2_gemm.cu): large static weights (fc
+  // layers) then need no per-call split pass and no hi/lo workspace.
+  const Tuning tu = tuning();
+  const bool k2_flo = algo == CGB_ALGO_EXPLICIT && prec == CGB_PREC_3XTF32 &&
+                      (tu.k2_flo > 0 || (tu.k2_flo == 0 && g.k_n * g.k * 4 > (int64_t(8) << 20)));
+  pl.direct_filters = (prec == CGB_PREC_TF32 || k2_flo) && g.k_n % 4 == 0 &&
                       (F == nullptr || reinterpret_cast<uintptr_t>(F) % 16 == 0);
   if (tf32_family(prec) && !pl.direct_filters)
     pl.f_bytes = align_up(pl.ldf * g.k * 4, 256) * (prec == CGB_PREC_3XTF32 ? 2 : 1);
@@ -432,9 +451,12 @@ static cgb_status conv_impl(int algo, int precision, const float* F, const float
     } else if (!Bhat && gather_supported(g) && ldf == g.k_n) {
       e = launch_tc_gather(f_hi, f_lo, I, O, g, split, s);
       g_last_path = 6;
+    } else if (Bhat) {  // explicit path: TMA-fed GEMM over the lowered matrix (K2)
+      e = launch_k2_gemm(f_hi, f_lo, ldf, Bhat, pl.ldb, O, g, split, s);
+      g_last_path = 2;
     } else {
-      e = launch_tc_conv(f_hi, f_lo, ldf, I, Bhat, pl.ldb, O, g, split, s);
-      g_last_path = Bhat ? 2 : 1;
+      e = launch_tc_conv(f_hi, f_lo, ldf, I, O, g, split, s);
+      g_last_path = 1;
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "conv kernel launch");

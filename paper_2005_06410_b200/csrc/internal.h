@@ -32,6 +32,7 @@ struct Tuning {
   int smem_pad_kb = 0;   // pad dynamic shared memory (shrinks the L1 carve-out)
   int tps = 0;           // shifted-window filter taps per stage hand-over (0 = by cost)
   int splitk = 0;        // split-K pieces for few-tile layers: -1 never, 0 auto, S forced
+  int k2_flo = 0;        // explicit 3xTF32: filter lo tile split in the kernel: -1 never, 0 by size, 1 always
   int64_t host_chunk_kb = 8192;  // host path: chunk size of the H2D || conv || D2H pipeline
   int host_no_bounce = 0;        // host path: DMA pageable buffers directly (no pinned ring)
   int host_copy_threads = 0;     // host path: memcpy pool size (0 = min(8, cores/2))
@@ -76,12 +77,24 @@ cudaError_t launch_im2col_f64(const double* I, double* B, int64_t ldb, const Con
 cudaError_t launch_filter_prep(const float* F, float* hi, float* lo, int64_t ldf, const ConvGeom& g,
                                cudaStream_t st);
 
-// K2/K3: tcgen05 kind::tf32 implicit GEMM. Filters are read by TMA from
-// (f_hi, f_lo) with leading dimension ldf (ldf*4 % 16 == 0). explicit_src selects
-// the explicit path (A rows from B with leading dimension ldb, ldb % 4 == 0).
-cudaError_t launch_tc_conv(const float* f_hi, const float* f_lo, int64_t ldf, const float* I,
-                           const float* explicit_src, int64_t ldb, float* O, const ConvGeom& g, bool split,
-                           cudaStream_t st);
+// K3: tcgen05 kind::tf32 implicit GEMM in the reference's row order (any geometry).
+// Filters are read by TMA from (f_hi, f_lo) with leading dimension ldf (ldf*4 % 16 == 0).
+cudaError_t launch_tc_conv(const float* f_hi, const float* f_lo, int64_t ldf, const float* I, float* O,
+                           const ConvGeom& g, bool split, cudaStream_t st);
+
+// K2 (k2_gemm.cu): the explicit path's GEMM over a lowered matrix Bhat (k x n, K-fastest,
+// ld = ldb with ldb % 4 == 0, 16-byte aligned), both operands TMA-fed. f_lo == nullptr
+// with split: the filter lo tile is computed in the kernel from the raw filters.
+cudaError_t launch_k2_gemm(const float* f_hi, const float* f_lo, int64_t ldf, const float* Bhat, int64_t ldb,
+                           float* O, const ConvGeom& g, bool split, cudaStream_t st);
+// 2-D TMA descriptor over Bhat (K x n, ld = ldb floats): box 32 rows of K x 128 columns,
+// 128-byte swizzle (the K-major UMMA A layout), out-of-range rows/columns read as zero.
+cudaError_t make_bhat_tmap(CUtensorMap* tm, const float* b, int64_t K, int64_t n, int64_t ldb);
+// Per-(device, stream) arrival counters (n ints, zero between launches) and partial-tile
+// workspace for split launches (shifted_conv.cu); false when the allocation fails.
+namespace sw {
+bool sk_buffers(cudaStream_t st, size_t n, size_t ws_bytes, int** counters, float** ws);
+}
 
 // 2-D TMA descriptor over a filter matrix (k_n x K, leading dimension ldf floats):
 // box 32 filters x 32 rows, 128-byte swizzle with 32-byte atoms (the MN-major

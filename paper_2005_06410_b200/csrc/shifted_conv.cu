@@ -1047,7 +1047,7 @@ static std::vector<void*> g_sk_retired;
 
 // Counters (n ints) and partial-tile workspace (ws_bytes) for a stream-K launch on st,
 // one set per (device, stream) so launches that may run concurrently never share one.
-static bool sk_buffers(cudaStream_t st, size_t n, size_t ws_bytes, int** counters, float** ws) {
+bool sk_buffers(cudaStream_t st, size_t n, size_t ws_bytes, int** counters, float** ws) {
   std::lock_guard<std::mutex> lk(g_sk_mu);
   int dev = 0;
   cudaGetDevice(&dev);

@@ -65,14 +65,126 @@ __global__ void __launch_bounds__(256) im2col_kernel(const float* __restrict__ I
   }
 }
 
+// Slab version for 16-byte-aligned B (the explicit path's workspace): a CTA stages the
+// input slab of one (image, h tile, w tile, channel block) in shared memory -- padding
+// zeros included, loaded with lanes along h (coalesced) -- then writes its piece of
+// every lowered column with lanes along r: one 16-byte store per lane, 512 contiguous
+// bytes per warp instruction, no bounds checks and no divisions in the write loop (the
+// r -> slab offset table is pixel-independent and built once per CTA).
+struct SlabArgs {
+  int32_t k_h, k_w, c_i, h_i, w_i, s, p, h_o, w_o, K;
+  int32_t CB, NCB, HT, NHT, WT, NWT, HP, HPpad, WS, RB;
+  int64_t ldb, plane;
+};
+
+__global__ void __launch_bounds__(256) im2col_slab_kernel(const float* __restrict__ I, float* __restrict__ B,
+                                                         SlabArgs a) {
+  extern __shared__ float slab_smem[];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  int64_t item = blockIdx.x;
+  const int cb = (int)(item % a.NCB); item /= a.NCB;
+  const int wt = (int)(item % a.NWT); item /= a.NWT;
+  const int ht = (int)(item % a.NHT);
+  const int i_b = (int)(item / a.NHT);
+  const int cbn = min(a.CB, a.c_i - cb * a.CB);                        // channels of this block
+  const int nrows = cb == a.NCB - 1 ? (int)a.ldb - cb * a.RB : a.RB;   // lowered rows of this block (% 4 == 0)
+  const int slab_floats = (a.CB * a.WS * a.HPpad + 3) & ~3;  // the table is read as int4
+  int32_t* table = reinterpret_cast<int32_t*>(slab_smem + slab_floats);
+  const int khw = a.k_h * a.k_w;
+  for (int r = tid; r < nrows; r += 256) {
+    int32_t off = -1;  // rows >= K (zero fill up to ldb)
+    if (cb * a.RB + r < a.K) {
+      const int c = r / khw, t = r - c * khw;
+      const int kw = t / a.k_h, kh = t - kw * a.k_h;
+      off = (c * a.WS + kw) * a.HPpad + kh;
+    }
+    table[r] = off;
+  }
+  const int h_base = ht * a.HT, w_base = wt * a.WT;
+  const int htn = min(a.HT, a.h_o - h_base), wtn = min(a.WT, a.w_o - w_base);
+  const int hp = (htn - 1) * a.s + a.k_h;  // slab rows actually read
+  const float* img = I + ((int64_t)i_b * a.c_i + (int64_t)cb * a.CB) * a.plane;
+  for (int row = warp; row < cbn * a.WS; row += 8) {
+    const int c = row / a.WS, wl = row - c * a.WS;
+    const int ww = w_base * a.s - a.p + wl;
+    const bool wok = (unsigned)ww < (unsigned)a.w_i;
+    const float* src = img + (int64_t)c * a.plane + (int64_t)ww * a.h_i + (h_base * a.s - a.p);
+    float* dst = slab_smem + row * a.HPpad;
+    for (int j = lane; j < hp; j += 32) {
+      const int hh = h_base * a.s - a.p + j;
+      dst[j] = (wok && (unsigned)hh < (unsigned)a.h_i) ? __ldg(src + j) : 0.0f;
+    }
+  }
+  __syncthreads();
+  const int npix = htn * wtn;
+  const int nch = nrows / 4;
+  const int4* table4 = reinterpret_cast<const int4*>(table);
+  for (int pix = warp; pix < npix; pix += 8) {
+    const int wl = pix / htn, hl = pix - wl * htn;
+    const int base = (wl * a.s) * a.HPpad + hl * a.s;
+    const int64_t col = (int64_t)(h_base + hl) + (int64_t)(w_base + wl) * a.h_o + (int64_t)i_b * a.h_o * a.w_o;
+    float* dst = B + col * a.ldb + (int64_t)cb * a.RB;
+    for (int ch = lane; ch < nch; ch += 32) {
+      const int4 o = table4[ch];
+      float4 v;
+      v.x = o.x < 0 ? 0.0f : slab_smem[base + o.x];
+      v.y = o.y < 0 ? 0.0f : slab_smem[base + o.y];
+      v.z = o.z < 0 ? 0.0f : slab_smem[base + o.z];
+      v.w = o.w < 0 ? 0.0f : slab_smem[base + o.w];
+      *reinterpret_cast<float4*>(dst + 4 * ch) = v;
+    }
+  }
+}
+
+static bool launch_im2col_slab(const float* I, float* B, int64_t ldb, const ConvGeom& g, cudaStream_t st,
+                               cudaError_t* err) {
+  SlabArgs a;
+  a.k_h = (int32_t)g.k_h; a.k_w = (int32_t)g.k_w; a.c_i = (int32_t)g.c_i; a.h_i = (int32_t)g.h_i;
+  a.w_i = (int32_t)g.w_i; a.s = (int32_t)g.s; a.p = (int32_t)g.p; a.h_o = (int32_t)g.h_o; a.w_o = (int32_t)g.w_o;
+  a.K = (int32_t)g.k; a.ldb = ldb; a.plane = g.h_i * g.w_i;
+  a.HT = (int32_t)std::min<int64_t>(g.h_o, 64);
+  a.NHT = (a.h_o + a.HT - 1) / a.HT;
+  a.WT = (int32_t)std::min<int64_t>(g.w_o, std::max(1, 32 / a.HT));
+  a.NWT = (a.w_o + a.WT - 1) / a.WT;
+  a.HP = (a.HT - 1) * a.s + a.k_h;
+  a.HPpad = a.HP | 1;
+  a.WS = (a.WT - 1) * a.s + a.k_w;
+  const int64_t per_c = (int64_t)a.WS * a.HPpad * 4;
+  const int64_t khw = g.k_h * g.k_w;
+  // channel block: whole c_i when it fits 48 KB, else a multiple of 4 channels (every
+  // block's first lowered row then stays 16-byte aligned)
+  int64_t cb = std::min<int64_t>(g.c_i, (48 * 1024) / per_c);
+  if (cb < g.c_i) cb = cb / 4 * 4;
+  if (cb < 1) return false;
+  a.CB = (int32_t)cb;
+  a.NCB = (int32_t)((g.c_i + cb - 1) / cb);
+  a.RB = (int32_t)(cb * khw);
+  const int64_t rows_last = ldb - (int64_t)(a.NCB - 1) * a.RB;
+  const int64_t table_rows = std::max<int64_t>(a.RB, rows_last);
+  const size_t smem = (size_t)((cb * per_c + 15) / 16 * 16) + (size_t)((table_rows + 3) / 4 * 4) * 4;
+  const int64_t blocks = g.b * a.NHT * a.NWT * a.NCB;
+  if (smem > 200 * 1024 || blocks > 0x7fffffffLL) return false;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(im2col_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  im2col_slab_kernel<<<(unsigned)blocks, 256, smem, st>>>(I, B, a);
+  count_launch();
+  *err = cudaGetLastError();
+  return true;
+}
+
 cudaError_t launch_im2col(const float* I, float* B, int64_t ldb, const ConvGeom& g, cudaStream_t st) {
+  const bool vec = (ldb % 4 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+  cudaError_t err = cudaSuccess;
+  if (vec && launch_im2col_slab(I, B, ldb, g, st, &err)) return err;
   Im2colArgs a;
   a.k_h = (int32_t)g.k_h; a.k_w = (int32_t)g.k_w; a.c_i = (int32_t)g.c_i; a.h_i = (int32_t)g.h_i;
   a.w_i = (int32_t)g.w_i; a.s = (int32_t)g.s; a.p = (int32_t)g.p; a.h_o = (int32_t)g.h_o; a.w_o = (int32_t)g.w_o;
   a.K = (int32_t)g.k; a.n = g.n; a.ldb = ldb; a.plane = g.h_i * g.w_i;
   const int64_t total = ((ldb + 3) / 4) * g.n;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
-  const bool vec = (ldb % 4 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
   if (vec)
     im2col_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(I, B, a);
   else

@@ -1,9 +1,9 @@
-// tc_conv.cu -- K2/K3: tcgen05 (kind::tf32) implicit-GEMM convolution for sm_100a.
+// tc_conv.cu -- K3: tcgen05 (kind::tf32) implicit-GEMM convolution for sm_100a in the
+// reference's row order (any geometry; the fallback of the fused path).
 //
-// Replaces the reference's five-loop BLIS GEMM driven by a PackingSource
-// (gemm.hpp:46-97) -- pack_b_im2col (im2col.hpp:177-262) for the fused path,
-// MatrixSource::pack_block (packing.hpp:89-113) for the explicit path -- and its
-// 8x12 micro-kernel (microkernel.hpp:20-38).
+// Replaces the reference's five-loop BLIS GEMM driven by pack_b_im2col
+// (gemm.hpp:46-97, im2col.hpp:177-262) and its 8x12 micro-kernel
+// (microkernel.hpp:20-38). The explicit path's GEMM over B-hat is k2_gemm.cu.
 //
 // GEMM orientation: M = output pixels (column c of the lowered matrix,
 // c = i_h + i_w*h_o + i_b*h_o*w_o), N = filters (k_n), K = k_h*k_w*c_i in the
@@ -14,8 +14,7 @@
 // Operands:
 //   A (pixels x K, K-major, 128B swizzle): gathered by 8 producer warps
 //     (register-staged: LDG -> [TF32 rounding | 3xTF32 hi/lo split] -> STS into the
-//     canonical swizzled layout). The lowered matrix never reaches HBM on the fused
-//     path; on the explicit path the rows come from B (ld = ldb).
+//     canonical swizzled layout). The lowered matrix never reaches HBM.
 //   B (K x filters, MN-major, 128B swizzle of 32-byte atoms): TMA boxes of 32 filters x 32 rows
 //     straight from F (k_n fastest is already MN-major), or from the hi/lo split.
 // Roles (320 threads): warps 0-7 A producers (warps 0-3 then run the epilogue on
@@ -53,7 +52,7 @@ struct Cfg {
 struct Args {
   int32_t k_n, k_h, k_w, c_i, h_i, w_i, s, p, h_o, w_o, K;
   int32_t KT;  // number of BK steps
-  int64_t n, ldb, plane;
+  int64_t n, plane;
   // mixed-radix decomposition of BK in (c, kw, kh) digits
   int32_t d_c, d_kw, d_kh;
 };
@@ -68,32 +67,18 @@ struct ChunkState {
   int32_t c, kw, kh, r;  // decomposition of the chunk's first row at the current stage
 };
 
-template <bool EXPLICIT>
-CGB_DEV void gather_chunk(const Args& a, const RowState& rs, const ChunkState& cs, const float* Bexp, int64_t P,
-                          float (&v)[4]) {
-  if (EXPLICIT) {
-    // rows >= K of a caller's B (ldb > k, gemm.hpp) are not part of the operand: bounded
-    // by K, not ldb (they would otherwise meet zero filter rows, and 0 * NaN/Inf = NaN)
-    if (rs.ok && cs.r + 3 < a.K) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(Bexp + P * a.ldb + cs.r));
-      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    } else {
+CGB_DEV void gather_chunk(const Args& a, const RowState& rs, const ChunkState& cs, float (&v)[4]) {
+  int32_t c = cs.c, kw = cs.kw, kh = cs.kh;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = (rs.ok && cs.r + e < a.K) ? __ldg(Bexp + P * a.ldb + cs.r + e) : 0.0f;
-    }
-  } else {
-    int32_t c = cs.c, kw = cs.kw, kh = cs.kh;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int32_t hh = rs.h0 + kh, ww = rs.w0 + kw;
-      float x = 0.0f;
-      if (rs.ok && cs.r + e < a.K && (unsigned)hh < (unsigned)a.h_i && (unsigned)ww < (unsigned)a.w_i)
-        x = __ldg(rs.base + c * a.plane + kw * a.h_i + kh);
-      v[e] = x;
-      if (++kh == a.k_h) {
-        kh = 0;
-        if (++kw == a.k_w) { kw = 0; ++c; }
-      }
+  for (int e = 0; e < 4; ++e) {
+    const int32_t hh = rs.h0 + kh, ww = rs.w0 + kw;
+    float x = 0.0f;
+    if (rs.ok && cs.r + e < a.K && (unsigned)hh < (unsigned)a.h_i && (unsigned)ww < (unsigned)a.w_i)
+      x = __ldg(rs.base + c * a.plane + kw * a.h_i + kh);
+    v[e] = x;
+    if (++kh == a.k_h) {
+      kh = 0;
+      if (++kw == a.k_w) { kw = 0; ++c; }
     }
   }
 }
@@ -111,10 +96,10 @@ CGB_DEV void advance_chunk(const Args& a, ChunkState& cs) {
   cs.kh = kh;
 }
 
-template <int BN, bool SPLIT, bool EXPLICIT>
+template <int BN, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap tmap_hi, const __grid_constant__ CUtensorMap tmap_lo,
-                   const float* __restrict__ I, const float* __restrict__ Bexp, float* __restrict__ O, Args a) {
+                   const float* __restrict__ I, float* __restrict__ O, Args a) {
   using C = Cfg<BN, SPLIT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -153,16 +138,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp < PRODUCER_WARPS) {
     // ------------------------------------------------------------ A producers
     RowState rs[2];
-    int64_t Prow[2];
     int rows[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       rows[q] = (lane % 8) + 8 * (warp + 8 * q);
       const int64_t P = m0 + rows[q];
-      Prow[q] = P;
       rs[q].ok = P < a.n;
       rs[q].h0 = 0; rs[q].w0 = 0; rs[q].base = I;
-      if (!EXPLICIT && rs[q].ok) {
+      if (rs[q].ok) {
         const int32_t hw = a.h_o * a.w_o;
         const int32_t i_b = (int32_t)(P / hw);
         const int32_t rem = (int32_t)(P - (int64_t)i_b * hw);
@@ -189,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int q = 0; q < 2; ++q)
 #pragma unroll
-        for (int v = 0; v < 2; ++v) gather_chunk<EXPLICIT>(a, rs[q], cs[v], Bexp, Prow[q], vals[q][v]);
+        for (int v = 0; v < 2; ++v) gather_chunk(a, rs[q], cs[v], vals[q][v]);
     };
     load_stage();
     for (int kt = 0; kt < a.KT; ++kt) {
@@ -309,30 +292,29 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int BN, bool SPLIT, bool EXPLICIT>
-cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float* I, const float* Bexp,
-                       float* O, const Args& a, int64_t n, int64_t k_n, cudaStream_t st) {
+template <int BN, bool SPLIT>
+cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O, const Args& a,
+                       int64_t n, int64_t k_n, cudaStream_t st) {
   using C = Cfg<BN, SPLIT>;
-  auto kern = tc_conv_kernel<BN, SPLIT, EXPLICIT>;
+  auto kern = tc_conv_kernel<BN, SPLIT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((n + BM - 1) / BM), (unsigned)((k_n + BN - 1) / BN));
-  kern<<<grid, THREADS, C::SMEM, st>>>(th, tl, I, Bexp, O, a);
+  kern<<<grid, THREADS, C::SMEM, st>>>(th, tl, I, O, a);
   count_launch();
   return cudaGetLastError();
 }
 
 }  // namespace tc
 
-cudaError_t launch_tc_conv(const float* f_hi, const float* f_lo, int64_t ldf, const float* I,
-                           const float* explicit_src, int64_t ldb, float* O, const ConvGeom& g, bool split,
-                           cudaStream_t st) {
+cudaError_t launch_tc_conv(const float* f_hi, const float* f_lo, int64_t ldf, const float* I, float* O,
+                           const ConvGeom& g, bool split, cudaStream_t st) {
   tc::Args a;
   a.k_n = (int32_t)g.k_n; a.k_h = (int32_t)g.k_h; a.k_w = (int32_t)g.k_w; a.c_i = (int32_t)g.c_i;
   a.h_i = (int32_t)g.h_i; a.w_i = (int32_t)g.w_i; a.s = (int32_t)g.s; a.p = (int32_t)g.p;
   a.h_o = (int32_t)g.h_o; a.w_o = (int32_t)g.w_o; a.K = (int32_t)g.k;
   a.KT = (int32_t)((g.k + tc::BK - 1) / tc::BK);
-  a.n = g.n; a.ldb = ldb; a.plane = g.h_i * g.w_i;
+  a.n = g.n; a.plane = g.h_i * g.w_i;
   {
     const int32_t khw = a.k_h * a.k_w;
     a.d_c = tc::BK / khw;
@@ -349,16 +331,10 @@ cudaError_t launch_tc_conv(const float* f_hi, const float* f_lo, int64_t ldf, co
   } else {
     tl = th;
   }
-  const bool ex = explicit_src != nullptr;
   const int64_t kn = g.k_n;
-#define CGB_TC_DISPATCH(BN)                                                                              \
-  if (split) {                                                                                           \
-    return ex ? tc::launch_cfg<BN, true, true>(th, tl, I, explicit_src, O, a, g.n, kn, st)               \
-              : tc::launch_cfg<BN, true, false>(th, tl, I, explicit_src, O, a, g.n, kn, st);             \
-  } else {                                                                                               \
-    return ex ? tc::launch_cfg<BN, false, true>(th, tl, I, explicit_src, O, a, g.n, kn, st)              \
-              : tc::launch_cfg<BN, false, false>(th, tl, I, explicit_src, O, a, g.n, kn, st);            \
-  }
+#define CGB_TC_DISPATCH(BN)                                                      \
+  return split ? tc::launch_cfg<BN, true>(th, tl, I, O, a, g.n, kn, st)          \
+               : tc::launch_cfg<BN, false>(th, tl, I, O, a, g.n, kn, st);
   if (kn <= 32) { CGB_TC_DISPATCH(32) }
   if (kn <= 64) { CGB_TC_DISPATCH(64) }
   if (kn <= 128) { CGB_TC_DISPATCH(128) }
