@@ -15,8 +15,11 @@
 //
 // Roles: warp 0 TMA producer (+TMEM alloc), warp 1 MMA issuer, warps 2-5 epilogue
 // (TMEM lane quadrant = warp % 4), 3xTF32 only: warps 6-13 "lo" warps. Persistent
-// grid, one ring of STAGES (A tile, filter tile) slots, two TMEM accumulator sets so
-// the epilogue of one tile overlaps the main loop of the next.
+// grid, one ring of STAGES (A tile, filter tile) slots filled by TMA -- as deep as shared
+// memory allows, since it has to cover the HBM latency -- plus, in 3xTF32, a short ring
+// of LOS lo slots written by the lo warps (they are consumed within one stage time);
+// two TMEM accumulator sets so the epilogue of one tile overlaps the main loop of the
+// next.
 //
 // 3xTF32: the tensor core truncates raw fp32 operands to TF32 (pinned by
 // tests/test_parity_gpu.py::test_tf32_truncates_raw_operands), so the TMA'd raw tile IS
@@ -42,16 +45,27 @@ constexpr int BK = 32;  // one 128-byte swizzle row of fp32
 constexpr int A_TILE = BM * BK * 4;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, EPI_WARP0 = 2, LO_WARP0 = 6, LO_WARPS = 8;
 
-template <int BN, bool SPLIT>
+// MODE 0: TF32. 1: 3xTF32, pre-split filter lo tiles arrive by TMA. 2: 3xTF32, the filter
+// lo tile is split in the kernel (FLO).
+template <int BN, int MODE>
 struct Cfg {
-  static constexpr int NS = SPLIT ? 2 : 1;
+  static constexpr bool SPLIT = MODE != 0;
+  static constexpr bool FLO = MODE == 2;
   static constexpr int B_TILE = BN * BK * 4;
-  static constexpr int STAGE = NS * (A_TILE + B_TILE);
-  static constexpr int STAGES_RAW = (216 * 1024) / STAGE;
+  static constexpr int STAGE = A_TILE + B_TILE * (MODE == 1 ? 2 : 1);  // TMA-filled: A raw, F raw[, F lo]
+  static constexpr int LO_SLOT = !SPLIT ? 0 : A_TILE + (FLO ? B_TILE : 0);  // lo-warp-filled: A lo[, F lo]
+  static constexpr int BUDGET = 216 * 1024;
+  // lo slots: a slot is busy from the split to the end of its stage's MMAs, about two
+  // stage times -- three slots where five TMA stages still fit beside them, else two
+  // while two stages fit, else one
+  static constexpr int LOS = !SPLIT ? 0
+                             : (BUDGET - 3 * LO_SLOT) / STAGE >= 5 ? 3
+                             : (BUDGET - 2 * LO_SLOT) / STAGE >= 2 ? 2 : 1;
+  static constexpr int STAGES_RAW = (BUDGET - LOS * LO_SLOT) / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int THREADS = 32 * (SPLIT ? LO_WARP0 + LO_WARPS : LO_WARP0);
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE + LOS * LO_SLOT + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(STAGES >= 2, "ring too shallow");
 };
 
@@ -63,7 +77,6 @@ struct Args {
   int32_t k_n, KT;  // filters, 32-row chunks of K
   int32_t m_tiles, n_tiles, S;
   int32_t nt_fast;  // work order: filter tile fastest (B-hat tile shared through L2) or pixel tile fastest
-  int32_t flo;      // 3xTF32: filter lo tile computed in the kernel (no pre-split filters)
   int32_t vec;      // O rows can take 32-byte (2) / 16-byte (1) vector stores
 };
 
@@ -106,20 +119,26 @@ CGB_DEV void store_row32(float* dst, const uint32_t (&r)[32], int ncols, int vec
   }
 }
 
-template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(Cfg<BN, SPLIT>::THREADS, 1)
+template <int BN, int MODE>
+__global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
     k2_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_hi,
                    const __grid_constant__ CUtensorMap tmap_lo, Args a) {
-  using C = Cfg<BN, SPLIT>;
+  using C = Cfg<BN, MODE>;
+  constexpr bool SPLIT = C::SPLIT, FLO = C::FLO;
+  constexpr int LOS = C::LOS > 0 ? C::LOS : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // stage s: [A raw/hi][A lo?][F raw/hi][F lo?]
-  auto a_tile = [&](int s, int part) { return smem + s * C::STAGE + part * A_TILE; };
-  auto b_tile = [&](int s, int part) { return smem + s * C::STAGE + C::NS * A_TILE + part * C::B_TILE; };
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  // stage s: [A raw][F raw][F lo (MODE 1)]; lo slot l: [A lo][F lo (MODE 2)]
+  auto a_tile = [&](int s) { return smem + s * C::STAGE; };
+  auto b_tile = [&](int s) { return smem + s * C::STAGE + A_TILE; };
+  auto b_lo_tma = [&](int s) { return smem + s * C::STAGE + A_TILE + C::B_TILE; };
+  auto a_lo = [&](int l) { return smem + C::STAGES * C::STAGE + l * C::LO_SLOT; };
+  auto b_lo_flo = [&](int l) { return smem + C::STAGES * C::STAGE + l * C::LO_SLOT + A_TILE; };
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE + C::LOS * C::LO_SLOT);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* lo_full = empty + C::STAGES;
-  uint64_t* tmem_full = lo_full + C::STAGES;  // [2]
+  uint64_t* lo_full = empty + C::STAGES;      // [LOS]
+  uint64_t* lo_empty = lo_full + 3;           // [LOS]
+  uint64_t* tmem_full = lo_empty + 3;         // [2]
   uint64_t* tmem_empty = tmem_full + 2;       // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
@@ -131,7 +150,10 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::THREADS, 1)
       for (int s = 0; s < C::STAGES; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], 1);
-        mbar_init(&lo_full[s], LO_WARPS);
+      }
+      for (int i = 0; i < 3; ++i) {
+        mbar_init(&lo_full[i], LO_WARPS);
+        mbar_init(&lo_empty[i], 1);
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&tmem_full[i], 1);
@@ -140,7 +162,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::THREADS, 1)
       fence_mbar_init();
       tma_prefetch_desc(&tmap_a);
       tma_prefetch_desc(&tmap_hi);
-      if (SPLIT) tma_prefetch_desc(&tmap_lo);
+      if (MODE == 1) tma_prefetch_desc(&tmap_lo);
     }
     __syncwarp();
     tmem_alloc(tmem_holder, C::TMEM_COLS);
@@ -154,8 +176,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::THREADS, 1)
   if (warp == TMA_WARP) {
     // ------------------------------------------------------------ TMA producer: B-hat tile + filter tile per stage
     if (elect_one()) {
-      const bool f_lo_tma = SPLIT && !a.flo;
-      const uint32_t bytes = A_TILE + C::B_TILE * (f_lo_tma ? 2 : 1);
+      constexpr uint32_t bytes = C::STAGE;
       uint32_t it = 0;
       for (int64_t w = blockIdx.x; w < a.items; w += gridDim.x) {
         const Item x = decode(a, w);
@@ -164,12 +185,12 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::THREADS, 1)
           const uint32_t ph = (it / C::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], bytes);
-          tma_load_2d(smem_u32(a_tile(s, 0)), &tmap_a, &full[s], kt * BK, x.mt * BM);
+          tma_load_2d(smem_u32(a_tile(s)), &tmap_a, &full[s], kt * BK, x.mt * BM);
 #pragma unroll
           for (int j = 0; j < (BN + 31) / 32; ++j) {
-            tma_load_2d(smem_u32(b_tile(s, 0)) + j * 4096, &tmap_hi, &full[s], x.nt * BN + 32 * j, kt * BK);
-            if (f_lo_tma)
-              tma_load_2d(smem_u32(b_tile(s, 1)) + j * 4096, &tmap_lo, &full[s], x.nt * BN + 32 * j, kt * BK);
+            tma_load_2d(smem_u32(b_tile(s)) + j * 4096, &tmap_hi, &full[s], x.nt * BN + 32 * j, kt * BK);
+            if (MODE == 1)
+              tma_load_2d(smem_u32(b_lo_tma(s)) + j * 4096, &tmap_lo, &full[s], x.nt * BN + 32 * j, kt * BK);
           }
         }
       }
@@ -190,7 +211,7 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::THREADS, 1)
           const uint32_t ph = (it / C::STAGES) & 1;
           mbar_wait_spin(&full[s], ph);
           tc_fence_after();
-          const uint32_t a_hi = smem_u32(a_tile(s, 0)), b_hi = smem_u32(b_tile(s, 0));
+          const uint32_t a_hi = smem_u32(a_tile(s)), b_hi = smem_u32(b_tile(s));
           // A: K-major SW128, k-step = +32 B inside the swizzle row; 8-row groups 1024 B apart.
           // F: MN-major SW128 with 32-byte atoms: k-step = +1024 B, 4-row groups 512 B apart,
           //    32-filter blocks 4096 B apart.
@@ -201,23 +222,26 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::THREADS, 1)
             mma_tf32(d, ad, bd, idesc, (kt != x.kt0 || kk != 0) ? 1u : 0u);
           }
           if (SPLIT) {
-            const uint32_t a_lo = smem_u32(a_tile(s, 1)), b_lo = smem_u32(b_tile(s, 1));
-            if (!a.flo) {  // pre-split filter lo arrived with the stage
+            if (MODE == 1) {  // pre-split filter lo arrived with the stage
+              const uint32_t b_lo = smem_u32(b_lo_tma(s));
 #pragma unroll
               for (int kk = 0; kk < BK / 8; ++kk)
                 mma_tf32(d, smem_desc(a_hi + kk * 32, 16, 1024),
                          smem_desc(b_lo + kk * 1024, 4096, 512, 0, kLayoutSW128_32B), idesc, 1);
             }
-            mbar_wait_spin(&lo_full[s], ph);
+            const int l = it % LOS;
+            mbar_wait_spin(&lo_full[l], (it / LOS) & 1);
             tc_fence_after();
+            const uint32_t al = smem_u32(a_lo(l));
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t bd = smem_desc(b_hi + kk * 1024, 4096, 512, 0, kLayoutSW128_32B);
-              mma_tf32(d, smem_desc(a_lo + kk * 32, 16, 1024), bd, idesc, 1);
-              if (a.flo)
+              mma_tf32(d, smem_desc(al + kk * 32, 16, 1024), bd, idesc, 1);
+              if (FLO)
                 mma_tf32(d, smem_desc(a_hi + kk * 32, 16, 1024),
-                         smem_desc(b_lo + kk * 1024, 4096, 512, 0, kLayoutSW128_32B), idesc, 1);
+                         smem_desc(smem_u32(b_lo_flo(l)) + kk * 1024, 4096, 512, 0, kLayoutSW128_32B), idesc, 1);
             }
+            mma_commit(&lo_empty[l]);
           }
           mma_commit(&empty[s]);
         }
@@ -278,12 +302,15 @@ __global__ void __launch_bounds__(Cfg<BN, SPLIT>::THREADS, 1)
       for (int kt = x.kt0; kt < x.kt1; ++kt, ++it) {
         const int s = it % C::STAGES;
         const uint32_t ph = (it / C::STAGES) & 1;
+        const int l = it % LOS;
+        // (spinning test_wait here measured 1.6x slower than the suspending try_wait)
+        mbar_wait_warp(&lo_empty[l], ((it / LOS) & 1) ^ 1);
         mbar_wait_warp(&full[s], ph);
-        split_tile(a_tile(s, 0), a_tile(s, 1), A_TILE);
-        if (a.flo) split_tile(b_tile(s, 0), b_tile(s, 1), C::B_TILE);
+        split_tile(a_tile(s), a_lo(l), A_TILE);
+        if (FLO) split_tile(b_tile(s), b_lo_flo(l), C::B_TILE);
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&lo_full[s]);
+        if (lane == 0) mbar_arrive(&lo_full[l]);
       }
     }
   }
@@ -321,11 +348,11 @@ __global__ void __launch_bounds__(256) k2_reduce_kernel(Args a) {
   }
 }
 
-template <int BN, bool SPLIT>
+template <int BN, int MODE>
 cudaError_t launch_cfg(const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, Args a, int sms,
                        cudaStream_t st) {
-  using C = Cfg<BN, SPLIT>;
-  auto kern = k2_gemm_kernel<BN, SPLIT>;
+  using C = Cfg<BN, MODE>;
+  auto kern = k2_gemm_kernel<BN, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   const Tuning tu = tuning();
@@ -386,7 +413,6 @@ cudaError_t launch_k2_gemm(const float* f_hi, const float* f_lo, int64_t ldf, co
   a.KT = (int32_t)((g.k + k2::BK - 1) / k2::BK);
   a.m_tiles = (int32_t)((g.n + k2::BM - 1) / k2::BM);
   a.nt_fast = g.n >= g.k_n;
-  a.flo = split && f_lo == nullptr;
   a.vec = 0;
   if (g.k_n % 8 == 0 && reinterpret_cast<uintptr_t>(O) % 32 == 0) a.vec = 2;
   else if (g.k_n % 4 == 0 && reinterpret_cast<uintptr_t>(O) % 16 == 0) a.vec = 1;
@@ -403,9 +429,11 @@ cudaError_t launch_k2_gemm(const float* f_hi, const float* f_lo, int64_t ldf, co
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t kn = g.k_n;
+  const int mode = !split ? 0 : (f_lo ? 1 : 2);
 #define CGB_K2_DISPATCH(BN)                                                   \
-  return split ? k2::launch_cfg<BN, true>(ta, th, tl, a, sms, st)             \
-               : k2::launch_cfg<BN, false>(ta, th, tl, a, sms, st);
+  return mode == 0   ? k2::launch_cfg<BN, 0>(ta, th, tl, a, sms, st)          \
+         : mode == 1 ? k2::launch_cfg<BN, 1>(ta, th, tl, a, sms, st)          \
+                     : k2::launch_cfg<BN, 2>(ta, th, tl, a, sms, st);
   if (kn <= 32) { CGB_K2_DISPATCH(32) }
   if (kn <= 64) { CGB_K2_DISPATCH(64) }
   if (kn <= 128) { CGB_K2_DISPATCH(128) }

@@ -67,16 +67,22 @@ __global__ void __launch_bounds__(256) im2col_kernel(const float* __restrict__ I
 
 // Slab version for 16-byte-aligned B (the explicit path's workspace): a CTA stages the
 // input slab of one (image, h tile, w tile, channel block) in shared memory -- padding
-// zeros included, loaded with lanes along h (coalesced) -- then writes its piece of
-// every lowered column with lanes along r: one 16-byte store per lane, 512 contiguous
-// bytes per warp instruction, no bounds checks and no divisions in the write loop (the
-// r -> slab offset table is pixel-independent and built once per CTA).
+// zeros included, filled by cp.async with lanes along h (coalesced, every load of the CTA
+// in flight at once) -- then writes its piece of every lowered column with lanes along
+// r: one 16-byte store per lane, 512 contiguous bytes per warp instruction. The r ->
+// slab offset map is pixel-independent: it is built once per CTA and each lane keeps the
+// offsets of its chunks in registers, so the write loop is 4 LDS + 1 STG per 16 bytes
+// with no bounds checks and no divisions. The kernel is issue-bound (ncu: 78% of the
+// issue slots), hence the care about instruction counts.
+//   V   elements per cp.async (2 needs an even h_i and an 8-byte aligned I)
+//   NCL chunks (16 B) per lane held in registers; 0 = any count (offsets re-read per pixel)
 struct SlabArgs {
   int32_t k_h, k_w, c_i, h_i, w_i, s, p, h_o, w_o, K;
   int32_t CB, NCB, HT, NHT, WT, NWT, HP, HPpad, WS, RB;
   int64_t ldb, plane;
 };
 
+template <int V, int NCL>
 __global__ void __launch_bounds__(256) im2col_slab_kernel(const float* __restrict__ I, float* __restrict__ B,
                                                          SlabArgs a) {
   extern __shared__ float slab_smem[];
@@ -90,50 +96,160 @@ __global__ void __launch_bounds__(256) im2col_slab_kernel(const float* __restric
   const int nrows = cb == a.NCB - 1 ? (int)a.ldb - cb * a.RB : a.RB;   // lowered rows of this block (% 4 == 0)
   const int slab_floats = (a.CB * a.WS * a.HPpad + 3) & ~3;  // the table is read as int4
   int32_t* table = reinterpret_cast<int32_t*>(slab_smem + slab_floats);
+  const int h_base = ht * a.HT, w_base = wt * a.WT;
+  const int htn = min(a.HT, a.h_o - h_base), wtn = min(a.WT, a.w_o - w_base);
+  const int hp = (htn - 1) * a.s + a.k_h;  // input rows the tile reads
+  const int h_first = h_base * a.s - a.p;  // input row of the tile's first tap (may be negative)
+  // slab column jj holds input row A0 + jj; A0 is V-aligned so that a cp.async never
+  // straddles the image edge and source and destination share their alignment
+  const int A0 = h_first & ~(V - 1);
+  const int j0 = h_first - A0;
   const int khw = a.k_h * a.k_w;
   for (int r = tid; r < nrows; r += 256) {
     int32_t off = -1;  // rows >= K (zero fill up to ldb)
     if (cb * a.RB + r < a.K) {
       const int c = r / khw, t = r - c * khw;
       const int kw = t / a.k_h, kh = t - kw * a.k_h;
-      off = (c * a.WS + kw) * a.HPpad + kh;
+      off = (c * a.WS + kw) * a.HPpad + kh + j0;
     }
     table[r] = off;
   }
-  const int h_base = ht * a.HT, w_base = wt * a.WT;
-  const int htn = min(a.HT, a.h_o - h_base), wtn = min(a.WT, a.w_o - w_base);
-  const int hp = (htn - 1) * a.s + a.k_h;  // slab rows actually read
   const float* img = I + ((int64_t)i_b * a.c_i + (int64_t)cb * a.CB) * a.plane;
-  for (int row = warp; row < cbn * a.WS; row += 8) {
-    const int c = row / a.WS, wl = row - c * a.WS;
-    const int ww = w_base * a.s - a.p + wl;
-    const bool wok = (unsigned)ww < (unsigned)a.w_i;
-    const float* src = img + (int64_t)c * a.plane + (int64_t)ww * a.h_i + (h_base * a.s - a.p);
-    float* dst = slab_smem + row * a.HPpad;
-    for (int j = lane; j < hp; j += 32) {
-      const int hh = h_base * a.s - a.p + j;
-      dst[j] = (wok && (unsigned)hh < (unsigned)a.h_i) ? __ldg(src + j) : 0.0f;
+  const uint32_t slab_s = smem_u32(slab_smem);
+  {
+    const int nv = (j0 + hp + V - 1) / V;  // cp.async per slab row
+    const int q8 = 8 / a.WS, r8 = 8 - q8 * a.WS;
+    int c = warp / a.WS, wl = warp - c * a.WS;
+    for (int row = warp; row < cbn * a.WS; row += 8) {
+      const int ww = w_base * a.s - a.p + wl;
+      const uint32_t dst = slab_s + (uint32_t)(row * a.HPpad) * 4u;
+      if ((unsigned)ww < (unsigned)a.w_i) {
+        const float* src = img + (int64_t)c * a.plane + (int64_t)ww * a.h_i + A0;
+        for (int q = lane; q < nv; q += 32) {
+          const bool ok = (unsigned)(A0 + V * q) < (unsigned)a.h_i;
+          const float* sp = src + (ok ? V * q : -A0);  // a valid address either way
+          if (V == 2)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + 8u * q), "l"(sp), "r"(ok ? 8u : 0u)
+                         : "memory");
+          else
+            cp_async_4(dst + 4u * q, sp, ok ? 4u : 0u);
+        }
+      } else {  // a padding column: zeros
+        for (int q = lane; q < nv * V; q += 32) slab_smem[row * a.HPpad + q] = 0.0f;
+      }
+      c += q8;
+      wl += r8;
+      if (wl >= a.WS) { wl -= a.WS; ++c; }
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+
   const int npix = htn * wtn;
   const int nch = nrows / 4;
   const int4* table4 = reinterpret_cast<const int4*>(table);
-  for (int pix = warp; pix < npix; pix += 8) {
-    const int wl = pix / htn, hl = pix - wl * htn;
-    const int base = (wl * a.s) * a.HPpad + hl * a.s;
-    const int64_t col = (int64_t)(h_base + hl) + (int64_t)(w_base + wl) * a.h_o + (int64_t)i_b * a.h_o * a.w_o;
-    float* dst = B + col * a.ldb + (int64_t)cb * a.RB;
-    for (int ch = lane; ch < nch; ch += 32) {
-      const int4 o = table4[ch];
-      float4 v;
-      v.x = o.x < 0 ? 0.0f : slab_smem[base + o.x];
-      v.y = o.y < 0 ? 0.0f : slab_smem[base + o.y];
-      v.z = o.z < 0 ? 0.0f : slab_smem[base + o.z];
-      v.w = o.w < 0 ? 0.0f : slab_smem[base + o.w];
-      *reinterpret_cast<float4*>(dst + 4 * ch) = v;
+  float* const Bblk = B + ((int64_t)h_base + (int64_t)w_base * a.h_o + (int64_t)i_b * a.h_o * a.w_o) * a.ldb +
+                      (int64_t)cb * a.RB + 4 * lane;
+  const int q8 = 8 / htn, r8 = 8 - q8 * htn;
+  int wl = warp / htn, hl = warp - wl * htn;
+  if constexpr (NCL > 0) {
+    // pixel-outer: the lane's chunk offsets live in registers
+    int4 o[NCL];
+#pragma unroll
+    for (int i = 0; i < NCL; ++i) {
+      const int ch = lane + 32 * i;
+      o[i] = ch < nch ? table4[ch] : make_int4(-2, -2, -2, -2);
+    }
+    for (int pix = warp; pix < npix; pix += 8) {
+      const float* sp = slab_smem + (wl * a.s) * a.HPpad + hl * a.s;
+      float* dst = Bblk + (int64_t)(hl + wl * a.h_o) * a.ldb;
+#pragma unroll
+      for (int i = 0; i < NCL; ++i) {
+        if (o[i].w >= 0) {  // offsets grow with r: the common, fully valid chunk
+          *reinterpret_cast<float4*>(dst + 128 * i) = make_float4(sp[o[i].x], sp[o[i].y], sp[o[i].z], sp[o[i].w]);
+        } else if (o[i].x != -2) {  // the chunk that crosses K (zero fill up to ldb)
+          float4 v;
+          v.x = o[i].x < 0 ? 0.0f : sp[o[i].x];
+          v.y = o[i].y < 0 ? 0.0f : sp[o[i].y];
+          v.z = o[i].z < 0 ? 0.0f : sp[o[i].z];
+          v.w = 0.0f;
+          *reinterpret_cast<float4*>(dst + 128 * i) = v;
+        }
+      }
+      wl += q8;
+      hl += r8;
+      if (hl >= htn) { hl -= htn; ++wl; }
+    }
+  } else {
+    for (int pix = warp; pix < npix; pix += 8) {
+      const float* sp = slab_smem + (wl * a.s) * a.HPpad + hl * a.s;
+      float* dst = Bblk + (int64_t)(hl + wl * a.h_o) * a.ldb;
+      for (int ch = lane; ch < nch; ch += 32) {
+        const int4 o = table4[ch];
+        float4 v;
+        v.x = o.x < 0 ? 0.0f : sp[o.x];
+        v.y = o.y < 0 ? 0.0f : sp[o.y];
+        v.z = o.z < 0 ? 0.0f : sp[o.z];
+        v.w = o.w < 0 ? 0.0f : sp[o.w];
+        *reinterpret_cast<float4*>(dst + 4 * (ch - lane)) = v;
+      }
+      wl += q8;
+      hl += r8;
+      if (hl >= htn) { hl -= htn; ++wl; }
     }
   }
+}
+
+// Row stride of the slab (>= need, a multiple of V) with the fewest shared-memory bank
+// conflicts in the write phase: lanes read the slab at table offsets of rows r = 4*lane + e.
+static int best_slab_stride(const SlabArgs& a, int need, int V, int rows) {
+  const int khw = a.k_h * a.k_w;
+  int best = (need + V - 1) / V * V, best_cost = 1 << 30;
+  for (int hp = best; hp < need + 34; hp += V) {
+    int cost = 0;
+    for (int g0 = 0; g0 < std::min(rows, 512); g0 += 128)
+      for (int e = 0; e < 4; ++e) {
+        int banks[32] = {0};
+        for (int l = 0; l < 32; ++l) {
+          const int r = g0 + 4 * l + e;
+          if (r >= rows) break;
+          const int c = r / khw, t = r - c * khw, kw = t / a.k_h, kh = t - kw * a.k_h;
+          ++banks[((c * a.WS + kw) * hp + kh) & 31];
+        }
+        int mx = 0;
+        for (int b = 0; b < 32; ++b) mx = std::max(mx, banks[b]);
+        cost += mx;
+      }
+    if (cost < best_cost) { best_cost = cost; best = hp; }
+  }
+  return best;
+}
+
+template <int V>
+static cudaError_t launch_slab_v(int ncl, unsigned blocks, size_t smem, const float* I, float* B, const SlabArgs& a,
+                                 cudaStream_t st) {
+#define CGB_SLAB_CASE(N)                                                                                     \
+  case N: {                                                                                                  \
+    auto kern = im2col_slab_kernel<V, N>;                                                                    \
+    if (smem > 48 * 1024 &&                                                                                  \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)  \
+      return cudaGetLastError();                                                                             \
+    kern<<<blocks, 256, smem, st>>>(I, B, a);                                                                \
+    break;                                                                                                   \
+  }
+  switch (ncl) {
+    CGB_SLAB_CASE(1) CGB_SLAB_CASE(2) CGB_SLAB_CASE(3) CGB_SLAB_CASE(4) CGB_SLAB_CASE(5) CGB_SLAB_CASE(6)
+    CGB_SLAB_CASE(8)
+    default: {
+      auto kern = im2col_slab_kernel<V, 0>;
+      if (smem > 48 * 1024 &&
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+        return cudaGetLastError();
+      kern<<<blocks, 256, smem, st>>>(I, B, a);
+    }
+  }
+#undef CGB_SLAB_CASE
+  return cudaGetLastError();
 }
 
 static bool launch_im2col_slab(const float* I, float* B, int64_t ldb, const ConvGeom& g, cudaStream_t st,
@@ -142,18 +258,20 @@ static bool launch_im2col_slab(const float* I, float* B, int64_t ldb, const Conv
   a.k_h = (int32_t)g.k_h; a.k_w = (int32_t)g.k_w; a.c_i = (int32_t)g.c_i; a.h_i = (int32_t)g.h_i;
   a.w_i = (int32_t)g.w_i; a.s = (int32_t)g.s; a.p = (int32_t)g.p; a.h_o = (int32_t)g.h_o; a.w_o = (int32_t)g.w_o;
   a.K = (int32_t)g.k; a.ldb = ldb; a.plane = g.h_i * g.w_i;
+  const int V = (g.h_i % 2 == 0 && reinterpret_cast<uintptr_t>(I) % 8 == 0) ? 2 : 1;
   a.HT = (int32_t)std::min<int64_t>(g.h_o, 64);
   a.NHT = (a.h_o + a.HT - 1) / a.HT;
-  a.WT = (int32_t)std::min<int64_t>(g.w_o, std::max(1, 32 / a.HT));
+  a.WT = (int32_t)std::min<int64_t>(g.w_o, std::max(1, 64 / a.HT));  // ~56-64 pixels per CTA
   a.NWT = (a.w_o + a.WT - 1) / a.WT;
   a.HP = (a.HT - 1) * a.s + a.k_h;
-  a.HPpad = a.HP | 1;
   a.WS = (a.WT - 1) * a.s + a.k_w;
+  a.HPpad = best_slab_stride(a, a.HP + V - 1, V, (int)std::min<int64_t>(g.k, 4096));
   const int64_t per_c = (int64_t)a.WS * a.HPpad * 4;
   const int64_t khw = g.k_h * g.k_w;
-  // channel block: whole c_i when it fits 48 KB, else a multiple of 4 channels (every
-  // block's first lowered row then stays 16-byte aligned)
-  int64_t cb = std::min<int64_t>(g.c_i, (48 * 1024) / per_c);
+  // channel block: at most 48 KB of slab and ~640 lowered rows (5 chunks per lane in
+  // registers); whole c_i when that fits, else a multiple of 4 channels (every block's
+  // first lowered row then stays 16-byte aligned)
+  int64_t cb = std::min<int64_t>({g.c_i, (48 * 1024) / per_c, std::max<int64_t>(640 / khw, 4)});
   if (cb < g.c_i) cb = cb / 4 * 4;
   if (cb < 1) return false;
   a.CB = (int32_t)cb;
@@ -164,14 +282,12 @@ static bool launch_im2col_slab(const float* I, float* B, int64_t ldb, const Conv
   const size_t smem = (size_t)((cb * per_c + 15) / 16 * 16) + (size_t)((table_rows + 3) / 4 * 4) * 4;
   const int64_t blocks = g.b * a.NHT * a.NWT * a.NCB;
   if (smem > 200 * 1024 || blocks > 0x7fffffffLL) return false;
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(im2col_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  im2col_slab_kernel<<<(unsigned)blocks, 256, smem, st>>>(I, B, a);
+  int ncl = (int)((table_rows / 4 + 31) / 32);  // chunks per lane
+  if (ncl == 7) ncl = 8;
+  if (ncl > 8) ncl = 0;
+  *err = V == 2 ? launch_slab_v<2>(ncl, (unsigned)blocks, smem, I, B, a, st)
+                : launch_slab_v<1>(ncl, (unsigned)blocks, smem, I, B, a, st);
   count_launch();
-  *err = cudaGetLastError();
   return true;
 }
 

@@ -1,5 +1,6 @@
 """One launch of a non-headline kernel for ncu (profiles/r02_*): python tools/ncu_cases.py CASE
-  explicit  56x56 64->64 b=128 through the explicit path: K1 im2col_kernel + K2 tc_conv_kernel
+  explicit  56x56 64->64 b=128 through the explicit path: K1 im2col_slab_kernel + K2 k2_gemm_kernel
+  explicit3x  the same in 3xTF32 (filter_prep + K1 + K2 with the lo warps)
   ffma      VGG conv1 (224^2 3->64) b=64 on the FFMA kernel (K4)
   fc6       VGG fc6 (4096 x 25088) at b=64 through cgb_gemm (TF32)
   stem      the 7x7/s2 stem at b=256 (w-im2col mode of the shifted-window kernel)
@@ -32,6 +33,9 @@ for _ in range(2):
     if case == "explicit":
         cp, F, I = layer("r50_3x3_56_64")
         cg.conv(F, I, cp, algo="explicit", precision="tf32")
+    elif case == "explicit3x":
+        cp, F, I = layer("r50_3x3_56_64")
+        cg.conv(F, I, cp, algo="explicit", precision="3xtf32")
     elif case == "ffma":
         cp, F, I = layer("vgg_224_3_64")
         cg.conv(F, I, cp, precision="ffma")

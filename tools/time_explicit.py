@@ -38,11 +38,12 @@ for name in ("r50_3x3_56_64", "r50_3x3_28_128", "r50_3x3_7_512", "r50_3x3_s2_56_
     bhat = 4 * ldb * n
     io = 4 * (I.numel() + F.numel() + m * n)
     line = f"{name:20s} b={cp['b']:3d} Bhat {bhat/1e6:7.1f} MB  K1 {t1:7.1f} us ({(bhat + 4*I.numel())/t1/1e3:6.0f} GB/s)"
-    for prec in ("tf32", "3xtf32"):
-        te = timed(lambda: cg.conv(F, I, cp, algo="explicit", precision=prec))
+    for prec, flo in (("tf32", 0), ("3xtf32", -1), ("3xtf32", 1)):
+        with cg.tuning(k2_flo=flo):
+            te = timed(lambda: cg.conv(F, I, cp, algo="explicit", precision=prec))
         tf = timed(lambda: cg.conv(F, I, cp, algo="fused", precision=prec))
         floor = (2 * bhat + io) / HBM * 1e6
-        line += f" | {prec}: explicit {te:7.1f} us (K2 ~{te - t1:6.1f}; floor {floor:5.0f}) fused {tf:6.1f}"
+        line += f" | {prec}{'/flo' if flo > 0 else ''}: explicit {te:7.1f} us (K2 ~{te - t1:6.1f}; floor {floor:5.0f}) fused {tf:6.1f}"
     print(line, flush=True)
     del B, F, I
 
