@@ -57,7 +57,8 @@ struct Cfg {
   static constexpr int BUDGET = 216 * 1024;
   // lo slots: a slot is busy from the split to the end of its stage's MMAs, about two
   // stage times -- three slots where five TMA stages still fit beside them, else two
-  // while two stages fit, else one
+  // while two stages fit (a third TMA stage instead of the second lo slot measured
+  // slower: fc6 3xTF32 216 vs 190 us), else one
   static constexpr int LOS = !SPLIT ? 0
                              : (BUDGET - 3 * LO_SLOT) / STAGE >= 5 ? 3
                              : (BUDGET - 2 * LO_SLOT) / STAGE >= 2 ? 2 : 1;
@@ -285,16 +286,26 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
     // ------------------------------------------------------------ lo warps: lo = rna_tf32(x - trunc_tf32(x))
     const int t = (warp - LO_WARP0) * 32 + lane;
     uint32_t it = 0;
+    // explicit shared-space accesses (through generic pointers the compiler emitted
+    // LD.E/ST.E and serialised every load behind the previous store), four 16-byte loads
+    // in flight per lane before the first store
     auto split_tile = [&](const uint8_t* src, uint8_t* dst, int bytes) {
-#pragma unroll 4
-      for (int off = t * 16; off < bytes; off += LO_WARPS * 32 * 16) {
-        const float4 x = *reinterpret_cast<const float4*>(src + off);
-        float4 l;
-        l.x = to_tf32(x.x - tf32_trunc(x.x));
-        l.y = to_tf32(x.y - tf32_trunc(x.y));
-        l.z = to_tf32(x.z - tf32_trunc(x.z));
-        l.w = to_tf32(x.w - tf32_trunc(x.w));
-        *reinterpret_cast<float4*>(dst + off) = l;
+      const uint32_t s0 = smem_u32(src) + t * 16, d0 = smem_u32(dst) + t * 16;
+      constexpr int STEP = LO_WARPS * 32 * 16;  // 4 KB per pass of the 8 warps
+      for (int off = 0; off < bytes; off += 4 * STEP) {
+        float v[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (off + u * STEP < bytes)
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v[u][0]), "=f"(v[u][1]), "=f"(v[u][2]), "=f"(v[u][3])
+                       : "r"(s0 + off + u * STEP));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (off + u * STEP < bytes)
+          st_shared_v4(d0 + off + u * STEP, to_tf32(v[u][0] - tf32_trunc(v[u][0])),
+                       to_tf32(v[u][1] - tf32_trunc(v[u][1])), to_tf32(v[u][2] - tf32_trunc(v[u][2])),
+                       to_tf32(v[u][3] - tf32_trunc(v[u][3])));
       }
     };
     for (int64_t w = blockIdx.x; w < a.items; w += gridDim.x) {
@@ -303,7 +314,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
         const int s = it % C::STAGES;
         const uint32_t ph = (it / C::STAGES) & 1;
         const int l = it % LOS;
-        // (spinning test_wait here measured 1.6x slower than the suspending try_wait)
+        // suspending try_wait, one polling lane per warp: spinning test_wait lanes measured
+        // 1.6x slower on the N = 64 shapes (their polls compete with the shared-memory-bound
+        // UMMAs) and no faster elsewhere
         mbar_wait_warp(&lo_empty[l], ((it / LOS) & 1) ^ 1);
         mbar_wait_warp(&full[s], ph);
         split_tile(a_tile(s), a_lo(l), A_TILE);
