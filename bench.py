@@ -469,11 +469,19 @@ def run_gpu_arm(args, world, rank, local):
     if args.scaling == "strong":
         lo, hi = shard_split(BATCH, rank, world)  # threads.hpp:20-25 split of the global batch
         b = hi - lo
+    if args.shard_of > 1:
+        # analysis aid on a one-GPU box: time the shard rank 0 of an N-way strong-scaling run
+        # would get (e.g. b=16 of 128 for N=8); the line is marked and is not a contract line
+        assert world == 1, "--shard-of is a single-process measurement"
+        lo, hi = shard_split(BATCH, 0, args.shard_of)
+        b = hi - lo
     tensors = make_layer_tensors(cg, torch, LAYERS, b, rank, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.l2 == "flush" else None
     clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     step_flops_local = sum(flops(cp) for _, cp, _, _, _ in tensors)
     total_flops = step_flops_local * world if args.scaling == "weak" else sum(flops(layer_cp(l, BATCH)) for l in LAYERS)
+    if args.shard_of > 1:
+        total_flops = step_flops_local
 
     modes = {}
     parity = {}
@@ -550,7 +558,11 @@ def run_gpu_arm(args, world, rank, local):
                    "launch": "one CUDA-graph replay of the 7 layer launches per step (programmatic dependent launch "
                              "between kernels); per-layer times from an eager pass",
                    "parallelism": f"batch-sharded dp{world} ({args.scaling} scaling), no collective in the timed "
-                                  f"region"},
+                                  f"region",
+                   **({"shard_of": args.shard_of,
+                       "note": f"ANALYSIS LINE, not a contract run: the rank-0 shard (b={b}) of a "
+                               f"{args.shard_of}-way strong-scaling split timed alone on one GPU; value = shard "
+                               f"FLOPs / shard step time"} if args.shard_of > 1 else {})},
         "roofline": {"bound": "tensor", "achieved": hm["achieved_tflops"], "peak": peak,
                      "unit": "TFLOP/s", "frac": hm["achieved_tflops"] / peak, "traffic": traffic,
                      "peak_src": pk["tf32_src"],
@@ -595,6 +607,8 @@ def main():
     ap.add_argument("--cpu-min-time", type=float, default=2.0)
     ap.add_argument("--ref-batch", type=int, default=0, help="reference arm batch per step (0 = the full b=128)")
     ap.add_argument("--no-parity", action="store_true", help="skip the fp64 parity pass after timing")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="analysis: time only the rank-0 shard of an N-way strong-scaling split on this GPU")
     ap.add_argument("--tune", default="", help='dispatch knobs for A/B runs, JSON, e.g. {"tps": 1}')
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup

@@ -109,8 +109,11 @@ cgb_status cgb_im2col(const float* I, const cgb_conv_params* cp, float* B, int64
 
 /* C (m x n) = A (m x k) * B (k x n), column-major, O overwritten (the reference
  * zero-fills C before gemm, bench.cpp:149-151). Dense A and C (lda == ldc == m),
- * ldb >= k. Runs the explicit-path tensor-core (or FFMA) kernel with B as the lowered
- * matrix; precision as for cgb_conv. */
+ * ldb >= k. Runs the explicit path's TMA-fed tensor-core GEMM (K2; FFMA for
+ * CGB_PREC_FFMA) with B as the lowered matrix; few-column shapes (fc layers) are split
+ * over K so every SM streams its share of A, partial tiles summed in a fixed order.
+ * In the fp32-accurate mode weights larger than 8 MB are split into hi/lo in shared
+ * memory (no workspace, no per-call pass over A). precision as for cgb_conv. */
 cgb_status cgb_gemm(int precision, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                     int64_t m, int64_t n, int64_t k, void* workspace, size_t workspace_bytes, void* stream);
 
@@ -165,7 +168,8 @@ uint64_t cgb_scratch_cached_bytes(void);
  * Keys: "sk" (stream-K: 0 never, 1 auto, 2 always), "tail" (tail tiles: 0/1/2), "pair"
  * (CTA pairs allowed), "cfg" (force a kernel candidate, -1 auto), "mt", "bn" (force
  * tile sizes, 0 auto), "tma_a", "tma_deep" (1x1-layer variants), "pstore", "pdl",
- * "verbose", "smem_pad_kb", "tps", "splitk", "host_chunk_kb", "host_no_bounce", "host_copy_threads",
+ * "verbose", "smem_pad_kb", "tps", "splitk", "k2_flo" (explicit 3xTF32: filter lo tile split in
+ * the kernel: -1 never, 0 by size, 1 always), "host_chunk_kb", "host_no_bounce", "host_copy_threads",
  * "debug" (profiling builds only). Every setting gives a correct result; unknown keys
  * return CGB_INVALID_ARGUMENT. The library reads no environment variables. */
 cgb_status cgb_set_tuning(const char* key, int64_t value);
