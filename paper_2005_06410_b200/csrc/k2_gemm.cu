@@ -357,7 +357,13 @@ __global__ void __launch_bounds__(256) k2_reduce_kernel(Args a) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[e] += v[e];
     }
-    *reinterpret_cast<float4*>(a.O + P * a.k_n + col) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    float* dst = a.O + P * a.k_n + col;
+    if (a.vec) {  // O 16-byte aligned
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = acc[e];
+    }
   }
 }
 
