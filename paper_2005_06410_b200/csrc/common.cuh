@@ -304,6 +304,14 @@ CGB_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// Arrive without release semantics: for barriers that only order tensor-memory or
+// register-held state (e.g. "accumulator drained" after tcgen05.wait::ld). A release
+// arrive at cluster scope first waits for every earlier global store of the thread to be
+// visible GPU-wide -- the epilogue's output stores, ~1 us under load.
+CGB_DEV void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
 CGB_DEV void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
                "r"(bytes)

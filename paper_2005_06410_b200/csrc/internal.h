@@ -20,7 +20,7 @@ namespace cgb {
 struct Tuning {
   int sk = 1;            // stream-K split of the last rounds: 0 never, 1 by fill, 2 whenever it fits
   int tail = 1;          // tail tiles: 0 never, 1 by cost, 2 whenever they fit
-  int pair = 1;          // CTA pairs (cta_group::2) allowed
+  int pair = 1;          // CTA pairs (cta_group::2): 0 never, 1 by policy, 2 also for the w-im2col layers
   int cfg = -1;          // force one shifted-window candidate (index into kCands)
   int mt = 0;            // force the M tile (subtiles of 128 rows)
   int bn = 0;            // force the filter tile (64, 128, 256)
@@ -32,6 +32,7 @@ struct Tuning {
   int smem_pad_kb = 0;   // pad dynamic shared memory (shrinks the L1 carve-out)
   int tps = 0;           // shifted-window filter taps per stage hand-over (0 = by cost)
   int splitk = 0;        // split-K pieces for few-tile layers: -1 never, 0 auto, S forced
+  int b_res = 1;         // shifted-window: keep the filters resident in the ring when they fit (0 = always stream)
   int k2_flo = 0;        // explicit 3xTF32: filter lo tile split in the kernel: -1 never, 0 by size, 1 always
   int64_t host_chunk_kb = 8192;  // host path: chunk size of the H2D || conv || D2H pipeline
   int host_no_bounce = 0;        // host path: DMA pageable buffers directly (no pinned ring)

@@ -92,6 +92,8 @@ struct Args {
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
   int32_t tps;        // taps per filter stage group (divides B_STAGES; see the filter TMA warp)
+  int32_t b_res;      // filters resident: CC*taps <= B_STAGES and one filter tile, so stage cc*taps+tap is
+                      // loaded once per CTA and never recycled (no per-tile filter hand-overs)
   int32_t pstore;     // epilogue stores: 1 lane pairs 64 B (default), 0 per-lane 32 B (CGB_SW_PSTORE=0)
   int32_t tma_a;      // 1x1 layers: A (pixels x channels) TMA'd MN-major straight from I, no staging
   int32_t wim;        // w-im2col mode: a row holds the k_w*c_i values of one output row's w-taps
@@ -604,7 +606,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t ph = (it / A_SLOTS) & 1;
           const uint32_t base_hi = smem_u32(a_slot(s, 0));
           const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
-          mbar_wait_warp(&a_empty[s], ph ^ 1);
+          // one chunk per tile here: the slot hand-over chain (commit -> producers ->
+          // forwarder -> MMA) is on the critical path, so the waits spin (a suspended
+          // try_wait wakes up late)
+          if (lane == 0) mbar_wait_spin(&a_empty[s], ph ^ 1);
+          __syncwarp();
           // One unit in flight per iteration: a second one (the regular loop's UPI = 2)
           // raised the register pressure of the two-unit kernels for every layer.
           constexpr int WU = 1;
@@ -712,7 +718,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j)
         for (int cc = cc0; cc < cc1; ++cc, ++it) {
           const int s = it % A_SLOTS;
-          mbar_wait(&a_ready[s], (it / A_SLOTS) & 1);
+          if (a.wim) mbar_wait_spin(&a_ready[s], (it / A_SLOTS) & 1);
+          else mbar_wait(&a_ready[s], (it / A_SLOTS) & 1);
           mbar_arrive_cluster(lead_a_full + s * 8);
         }
     }
@@ -735,6 +742,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       const uint32_t b0_hi = smem_u32(b_slot(0, 0)), b0_lo = smem_u32(b_slot(0, SPLIT ? 1 : 0));
       int tile, cc0, cc1;
+      if (a.b_res) {
+        // resident filters: every (chunk, tap) stage once, each on its own barrier (phase 0)
+        const int n0 = (int)rank * C::NB;
+        for (int cc = 0; cc < a.CC; ++cc)
+          for (int tap = 0; tap < a.taps; ++tap) {
+            const int st_i = cc * a.taps + tap;
+            if (rank == 0) mbar_arrive_expect_tx(&b_full[st_i], bytes);
+            const uint32_t stage_off = (uint32_t)st_i * C::NS * C::B_TILE;
+#pragma unroll
+            for (int j = 0; j < C::NB / 32; ++j) {
+              if (PAIR) {
+                tma_load_3d_2sm(b0_hi + stage_off + j * 4096, &tmap_hi, lead_b_full + st_i * 8, n0 + 32 * j, tap, cc * BK);
+                if (SPLIT)
+                  tma_load_3d_2sm(b0_lo + stage_off + j * 4096, &tmap_lo, lead_b_full + st_i * 8, n0 + 32 * j, tap,
+                                  cc * BK);
+              } else {
+                tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[st_i], n0 + 32 * j, tap, cc * BK);
+                if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[st_i], n0 + 32 * j, tap, cc * BK);
+              }
+            }
+          }
+      }
       int ait = 0;  // TMA-fed A: chunk counter (window slot ring)
       for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
         const int n0 = (tile / a.m_tiles) * BN + (int)rank * C::NB;
@@ -759,7 +788,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             ++ait;
           }
-          for (int tap = 0; tap < a.taps; ++tap) {
+          for (int tap = 0; tap < a.taps && !a.b_res; ++tap) {
             // WAR on own smem: CTA scope suffices. A suspending try_wait, not a spin: the
             // ring is deep enough to hide the wake-up, and the spinning thread took issue
             // slots from the producer warps of its sub-partition (BN = 256 layers 0.5-1%).
@@ -796,7 +825,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      if (gq != 0) close_group(gb);  // a last, partial group
+      if (gq != 0 && !a.b_res) close_group(gb);  // a last, partial group
     }
   } else if (warp == MMA_WARP) {
     // ---------------------------------------------------------------- MMA issue
@@ -837,6 +866,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint64_t b_stage_units = (uint64_t)(C::NS * C::B_TILE) >> 4;
       const bool full_steps = a.ksteps == BK / 8;  // every k-step issued (all but w-im2col rows)
       int tile, cc0, cc1;
+      if (a.b_res) {  // resident filters: all stages land once (phase 0), then no filter waits at all
+        for (int i = 0; i < a.CC * a.taps; ++i) mbar_wait_spin(&b_full[i], 0);
+        tc_fence_after();
+      }
       for (; seg_get(a, gid, t, tile, cc0, cc1); ++t) {
         const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
         const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
@@ -863,7 +896,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             unsigned long long c2 = st ? clock64() : 0;
             // TMA completion bytes of both halves land on this (leader's) barrier; the
             // UMMA reads the data through the async proxy, so a CTA-scope wait suffices.
-            if (gq == 0) {
+            if (a.b_res) {
+              bs = cc * a.taps + tap;  // loaded once, waited for before the first tile
+            } else if (gq == 0) {
               mbar_wait_spin(&b_full[gb], gph);
               tc_fence_after();
             }
@@ -880,10 +915,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                 issue_tap<MT2, BN, SPLIT, PAIR, BK / 8>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first);
               else if (full_steps && mtc == MT4)
                 issue_tap<MT4, BN, SPLIT, PAIR, BK / 8>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first);
+              // w-im2col rows (stem: 3 k-steps per tap, VGG conv1: 2): unrolled batches too --
+              // with one chunk of 7 or 3 taps per tile the issuing thread is the critical path
+              else if (BN == 64 && a.ksteps == 3 && mtc == MT)
+                issue_tap<MT, BN, SPLIT, PAIR, 3>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first);
+              else if (BN == 64 && a.ksteps == 2 && mtc == MT)
+                issue_tap<MT, BN, SPLIT, PAIR, 2>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first);
               else
                 issue_tap_partial<MT, BN, SPLIT, PAIR>(d_base, at, at_lo, bt, bt_lo, idesc, a_kstep, first, mtc,
                                                        a.ksteps);
             }
+            if (a.b_res) continue;
             if (gq == G - 1) {
               if (PAIR) mma_commit_mc2(&b_empty[gb], 3);
               else mma_commit(&b_empty[gb]);
@@ -922,7 +964,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int n0 = (tile / a.m_tiles) * BN;
       unsigned long long e0 = CGB_DBG(64) ? clock64() : 0;
       if (PAIR) {
-        if (lane == 0) mbar_wait(&t_full[acc_set], acc_ph);
+        if (lane == 0) {
+          if (a.wim) mbar_wait_spin(&t_full[acc_set], acc_ph);
+          else mbar_wait(&t_full[acc_set], acc_ph);
+        }
         __syncwarp();
       } else {
         mbar_wait_warp(&t_full[acc_set], acc_ph);
@@ -1006,7 +1051,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (PAIR) mbar_arrive_cluster(lead_t_empty + acc_set * 8);
+        // relaxed: the barrier only hands the drained accumulator set (tcgen05.wait::ld done,
+        // tcgen05.fence above) back to the MMA issuer; a release here would first wait for
+        // this tile's output stores to become visible GPU-wide
+        if (PAIR && CGB_DBG(128)) mbar_arrive_cluster(lead_t_empty + acc_set * 8);  // A/B: the old release arrive
+        else if (PAIR) mbar_arrive_cluster_relaxed(lead_t_empty + acc_set * 8);
         else mbar_arrive(&t_empty[acc_set]);
       }
       if (CGB_DBG(64)) epi_busy += clock64() - e1;
@@ -1115,6 +1164,10 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   constexpr int pair_rows = (PAIR ? 2 : 1) * MT * 128;
   a.m_tiles = (int32_t)((a.Mp + pair_rows - 1) / pair_rows);
   a.n_tiles = (a.k_n + BN - 1) / BN;
+  // Filters resident in the ring (no recycling, no per-tile hand-overs): when every
+  // (chunk, tap) stage of the one filter tile fits -- the w-im2col layers (stem: 7 taps,
+  // VGG conv1: 3), short 1x1 layers.
+  a.b_res = tu.b_res != 0 && a.CC * a.taps <= B_STAGES && a.n_tiles == 1 && !(tu.debug & 8);
   size_t smem = base_smem;
   if (tu.smem_pad_kb > 0)  // profiling: shrink the L1 carve-out
     smem = std::max<size_t>(smem, (size_t)tu.smem_pad_kb * 1024);
@@ -1387,6 +1440,7 @@ static const Cand kCands[] = {
     {2, 256, 0, 4, 4, 1, 1}, {2, 128, 0, 4, 6, 1, 1},
     // probes (tuning cfg only)
     {1, 128, 0, 2, 6, 1, 2}, {1, 256, 0, 2, 3, 1, 2}, {1, 256, 0, 2, 4, 1, 2},
+    {2, 64, 0, 2, 8, 0, 1},  // single CTA with a ring that holds the stem's 7 taps resident
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
@@ -1394,6 +1448,7 @@ constexpr int kFirstUpi2Cand = 38;
 constexpr int kFirstSplit2Cand = 43;  // 3xTF32 with two window slots
 constexpr int kFirstTmaACand = 48;   // deep A rings, tried first for 1x1 layers
 constexpr int kFirstProbeCand = 50;  // candidates from here on are CGB_SW_CFG probes only
+constexpr int kWimCand = 53;         // the w-im2col layers' single-CTA kernel (dispatch)
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st, const Tuning& tu) {
@@ -1453,6 +1508,7 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(50, 1, 128, false, 2, 6, true, 2)
     CGB_SW_CASE(51, 1, 256, false, 2, 3, true, 2)
     CGB_SW_CASE(52, 1, 256, false, 2, 4, true, 2)
+    CGB_SW_CASE(53, 2, 64, false, 2, 8, false, 1)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -1471,9 +1527,22 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
     if (i < kNumCands && kCands[i].bn == bn && kCands[i].split == (int)split)
       return launch_cand(i, th, tl, I, O, a, st, tu);
   }
+  // w-im2col layers (one chunk of k_h taps per tile: ~1 us of UMMAs between hand-overs):
+  // single CTAs -- CTA-scope barriers instead of the pair's cluster-scope hand-overs --
+  // with the filters resident in the ring (b_res). Stem: 356 (pair) -> 345 (single CTA,
+  // 6 stages) -> 310 us (8 stages, all 7 taps resident); VGG conv1 214 -> 201 us.
+  if (a.wim && !split && tu.pair != 2) {
+    if (a.taps > 6 && bn == 64) {
+      cudaError_t e = launch_cand(kWimCand, th, tl, I, O, a, st, tu);
+      if (e != cudaErrorNotSupported) {
+        if (tu.verbose) fprintf(stderr, "[cgb] shifted cand %d (w-im2col, single CTA, resident filters)\n", kWimCand);
+        return e;
+      }
+    }
+  }
   // Preference (measured, tools/sweep_cfg.sh): CTA pairs first (CGB_SW_PAIR=0 disables),
   // then a double-buffered window (A slots = 2), then the M tile the cost model picks.
-  const bool allow_pair = tu.pair != 0;
+  const bool allow_pair = tu.pair != 0 && !(a.wim && !split && tu.pair != 2);
   // passes: pairs with a double-buffered window, pairs with any, single CTAs likewise
   for (int pass = 0; pass < 4; ++pass) {
     const int want_pair = pass < 2 ? 1 : 0;

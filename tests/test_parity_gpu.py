@@ -616,3 +616,28 @@ def test_split_k(orc, case, prec):
             b = to_host(cg.conv(dF, dI, cp, precision=prec))
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), S
         assert per_output_error(a, ref, scale) <= TOL[prec], (S, per_output_error(a, ref, scale))
+
+
+# ---------------------------------------------------------------- resident filters, w-im2col dispatch
+@pytest.mark.parametrize("cp", [
+    dict(k_n=64, k_h=7, k_w=7, c_i=3, h_i=40, w_i=36, b=3, s=2, p=3),    # the stem's shape: 7 taps resident
+    dict(k_n=64, k_h=3, k_w=3, c_i=3, h_i=30, w_i=30, b=2, s=1, p=1),    # VGG conv1's shape: 3 taps
+    dict(k_n=128, k_h=1, k_w=1, c_i=64, h_i=12, w_i=12, b=5, s=1, p=0),  # 1x1, two chunks resident (TMA-fed A)
+    dict(k_n=64, k_h=1, k_w=1, c_i=96, h_i=7, w_i=7, b=9, s=1, p=0),     # 1x1 staged windows, three chunks
+])
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_resident_filters_bitwise(orc, cp, prec):
+    """Filters kept resident in the ring (loaded once per CTA, no per-tile hand-overs) feed
+    the same bits to the same UMMAs as the streamed ring; the w-im2col layers' single-CTA
+    dispatch and the CTA-pair kernels (pair=2) both meet the bar."""
+    F, I = rand_inputs(cp, 4711, stem=cp["c_i"] == 3)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    Fd, Id = to_dev(F), to_dev(I)
+    outs = {}
+    for pair in (1, 2):
+        for br in (0, 1):
+            with cg.tuning(b_res=br, pair=pair):
+                outs[(pair, br)] = to_host(cg.conv(Fd, Id, cp, precision=prec))
+            assert per_output_error(outs[(pair, br)], ref, scale) <= TOL[prec], (pair, br)
+        assert np.array_equal(outs[(pair, 0)].view(np.uint32), outs[(pair, 1)].view(np.uint32)), pair
