@@ -128,26 +128,47 @@ inline void fast_div_magic(uint32_t d, uint32_t& m, uint32_t& p) {
 // role walks the same sequence; the state is just the segment index j (registers are
 // the binding resource of this kernel).
 CGB_DEV int64_t sk_begin(const Args& a, int g) { return (int64_t)g * a.sk_units / a.groups; }
-CGB_DEV bool seg_get(const Args& a, int gid, int j, int& tile, int& cc0, int& cc1) {
-  const int ub = (int)sk_begin(a, gid), ue = (int)sk_begin(a, gid + 1);
-  const int npieces = ue > ub ? (ue - 1) / a.CC - ub / a.CC + 1 : 0;
-  if (j < npieces) {
-    const int t0 = ub / a.CC + j;
-    const int us = j == 0 ? ub : t0 * a.CC;
+// The per-group constants of the sequence, computed once per role (seg_init): the per-tile
+// step (seg_at) is then free of integer divisions -- with one short chunk per tile (the
+// w-im2col layers: ~1 us of UMMAs) the two 64-bit and four 32-bit divisions of a
+// from-scratch lookup were ~1500 cycles per tile on the MMA issuing thread's critical path.
+struct Seg {
+  int ub, ue;      // this group's stream-K unit range
+  int t0;          // first split tile (ub / CC)
+  int npieces;     // pieces of split tiles
+  int ndp;         // whole tiles
+  int tbase;       // first whole tile of group 0 (sk_units / CC)
+};
+CGB_DEV Seg seg_init(const Args& a, int gid) {
+  Seg s;
+  s.ub = (int)sk_begin(a, gid);
+  s.ue = (int)sk_begin(a, gid + 1);
+  s.t0 = s.ub / a.CC;
+  s.npieces = s.ue > s.ub ? (s.ue - 1) / a.CC - s.t0 + 1 : 0;
+  s.ndp = gid < a.dp_tiles ? (a.dp_tiles - gid + a.groups - 1) / a.groups : 0;
+  s.tbase = a.sk_units / a.CC;
+  return s;
+}
+CGB_DEV bool seg_at(const Args& a, const Seg& s, int gid, int j, int& tile, int& cc0, int& cc1) {
+  if (j < s.npieces) {
+    const int t0 = s.t0 + j;
+    const int us = j == 0 ? s.ub : t0 * a.CC;
     tile = t0;
     cc0 = us - t0 * a.CC;
-    cc1 = min(a.CC, ue - t0 * a.CC);
+    cc1 = min(a.CC, s.ue - t0 * a.CC);
     return true;
   }
-  j -= npieces;
-  const int ndp = gid < a.dp_tiles ? (a.dp_tiles - gid + a.groups - 1) / a.groups : 0;
-  if (j < ndp) {
-    tile = a.sk_units / a.CC + gid + j * a.groups;
+  j -= s.npieces;
+  if (j < s.ndp) {
+    tile = s.tbase + gid + j * a.groups;
     cc0 = 0;
     cc1 = a.CC;
     return true;
   }
   return false;
+}
+CGB_DEV bool seg_get(const Args& a, int gid, int j, int& tile, int& cc0, int& cc1) {
+  return seg_at(a, seg_init(a, gid), gid, j, tile, cc0, cc1);
 }
 // group whose stream-K range holds unit x
 CGB_DEV int sk_group_of(const Args& a, int x) {
@@ -177,7 +198,7 @@ CGB_DEV void wim_row(const Args& a, const float* src, int32_t w0, float (&v)[32]
 template <int MT, bool PAIR>
 CGB_DEV void tile_rows(const Args& a, int tile, uint32_t rank, int32_t& m0, int& mtc) {
   constexpr int P = PAIR ? 2 : 1;
-  const int32_t mi = tile % a.m_tiles;
+  const int32_t mi = a.n_tiles == 1 ? tile : tile % a.m_tiles;
   if (a.tail_mt && mi >= a.m_full) {
     mtc = a.tail_mt;
     m0 = a.m_full * (P * MT * 128) + (mi - a.m_full) * (P * a.tail_mt * 128) + (int32_t)rank * a.tail_mt * 128;
@@ -596,7 +617,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       // ---- w-im2col rows (low-channel layers): row (h-phase pha, hq, wo, image) holds
       // I(s*hq + pha - p, s*wo + kw - p, c) at element j = c + c_i*kw (zero past k_w*c_i and
       // in the padding); only the k_h taps are row shifts. One chunk per tile.
-      for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
+      const Seg sg1 = seg_init(a, gid);
+      for (int j = 0; seg_at(a, sg1, gid, j, tile, cc0, cc1); ++j) {
         int32_t m0;
         int mtc;
         tile_rows<MT, PAIR>(a, tile, rank, m0, mtc);
@@ -657,7 +679,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (lane == 0) mbar_arrive(PAIR ? &a_ready[s] : &a_full[s]);
         }
       }
-    } else
+    } else {
+    // (from-scratch lookup here: these producers are the register-tightest path, and their
+    // tiles carry whole chunks of staging work)
     for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
       int32_t m0;
       int mtc;
@@ -708,6 +732,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    }
     if (CGB_DBG(64) && warp == 0 && lane == 0) a.stats[blockIdx.x * 16 + 13] = gtimer();
   } else if (warp == FWD_WARP) {
     // ---------------------------------------------------------------- window forwarder
@@ -715,7 +740,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // chunk here keeps it off the producer warps (the bottleneck of staging-bound layers).
     if (PAIR && lane == 0 && !a.tma_a) {
       int it = 0, tile, cc0, cc1;
-      for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j)
+      const Seg sg3 = seg_init(a, gid);
+      for (int j = 0; seg_at(a, sg3, gid, j, tile, cc0, cc1); ++j)
         for (int cc = cc0; cc < cc1; ++cc, ++it) {
           const int s = it % A_SLOTS;
           if (a.wim) mbar_wait_spin(&a_ready[s], (it / A_SLOTS) & 1);
@@ -765,7 +791,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
       }
       int ait = 0;  // TMA-fed A: chunk counter (window slot ring)
-      for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
+      const Seg sg4 = seg_init(a, gid);
+      for (int j = 0; seg_at(a, sg4, gid, j, tile, cc0, cc1); ++j) {
         const int n0 = (tile / a.m_tiles) * BN + (int)rank * C::NB;
         int32_t am0 = 0;
         int amtc = 0;
@@ -870,7 +897,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < a.CC * a.taps; ++i) mbar_wait_spin(&b_full[i], 0);
         tc_fence_after();
       }
-      for (; seg_get(a, gid, t, tile, cc0, cc1); ++t) {
+      const Seg sg5 = seg_init(a, gid);
+      for (; seg_at(a, sg5, gid, t, tile, cc0, cc1); ++t) {
         const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
         const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
         int32_t m0u;
@@ -955,7 +983,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     unsigned long long epi_wait = 0, epi_busy = 0;
     int t = 0;
     int tile, cc0, cc1;
-    for (; seg_get(a, gid, t, tile, cc0, cc1); ++t) {
+    const Seg sg6 = seg_init(a, gid);
+    for (; seg_at(a, sg6, gid, t, tile, cc0, cc1); ++t) {
       const int acc_set = C::ACC_SETS == 2 ? (t & 1) : 0;
       const uint32_t acc_ph = C::ACC_SETS == 2 ? ((t >> 1) & 1) : (t & 1);
       int32_t m0;
@@ -968,6 +997,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (a.wim) mbar_wait_spin(&t_full[acc_set], acc_ph);
           else mbar_wait(&t_full[acc_set], acc_ph);
         }
+        __syncwarp();
+      } else if (a.wim) {  // ~1 us of UMMAs per tile: a suspended try_wait wakes up too late
+        if (lane == 0) mbar_wait_spin(&t_full[acc_set], acc_ph);
         __syncwarp();
       } else {
         mbar_wait_warp(&t_full[acc_set], acc_ph);

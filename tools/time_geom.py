@@ -30,3 +30,12 @@ torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / reps
 fl = 2 * k_n * h_o * w_o * b * k * k * c_i
 print(f"{sys.argv[1:8]} {prec} {cg.last_path()} {us:.1f} us {fl / us / 1e6:.1f} TFLOPS")
+if int(os.environ.get("CGB_DEBUG_SW", "0")) & 64:
+    import numpy as np
+    buf = np.zeros((148, 16), dtype=np.uint64)
+    cg.lib.cgb_debug_sw_stats(buf.ctypes.data, 148)
+    lead = buf[:, 4] > 0  # CTAs whose MMA thread ran
+    tot, wt, wa, wb, nt, ew, eb = [buf[:, i].astype(np.float64) for i in range(7)]
+    print(f"  MMA thread cycles: total mean {tot[lead].mean():.0f}; wait t_empty {wt[lead].mean():.0f} a_full "
+          f"{wa[lead].mean():.0f} b_full {wb[lead].mean():.0f}; segments {nt[lead].mean():.1f}; epilogue wait "
+          f"{ew[lead].mean():.0f} busy {eb[lead].mean():.0f}")
