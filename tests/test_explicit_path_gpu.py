@@ -125,3 +125,53 @@ def test_fc_gemm_takes_no_filter_workspace_for_large_weights():
     cg.gemm(At, Bt, precision="3xtf32")
     torch.cuda.synchronize()
     assert cg.scratch_peak_bytes() == 0
+
+
+# ---------------------------------------------------------------- full size (the shapes the profiles quote)
+FULLSIZE_EXPLICIT = ["r50_3x3_56_64", "r50_3x3_s2_56_128", "r50_3x3_7_512", "pw_14_1024_256"]
+
+
+@pytest.mark.parametrize("name", FULLSIZE_EXPLICIT)
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_explicit_fullsize_fp64(name, prec):
+    """The explicit path (K1 slab im2col + K2 TMA-fed GEMM) at the BASELINE layers' stated
+    batch -- thousands of pixel tiles per CTA round, the lowered matrix up to 0.9 GB --
+    against an fp64 recomputation of every output (tests/fp64ref.py), and K1's lowered
+    matrix bit for bit against the oracle on two images."""
+    from paper_2005_06410_b200 import configs
+    from fp64ref import per_output_error_fp64
+    by = {l[0]: (cp, d) for _, l, cp, d in configs.all_layers()}
+    cp, dist = by[name]
+    F, I = configs.make_tensors(torch, cg.empty_tensor4, cp, dist, configs.layer_seed(name))
+    O = cg.conv(F, I, cp, algo="explicit", precision=prec)
+    assert cg.last_path() == "tcgen05-explicit"
+    err = per_output_error_fp64(torch, F, I, O, cp)
+    assert err <= TOL[prec], (name, prec, err)
+    if prec == "tf32":
+        m, n, k = cg.gemm_dims(cp)
+        ldb = (k + 3) // 4 * 4
+        B = cg.im2col(I, cp, ldb=ldb)  # (k, n) view, column stride ldb
+        per_img = n // cp["b"]
+        orc = Restatement()
+        for i in (0, cp["b"] - 1):
+            img = I[..., i:i + 1]
+            flat = img.permute(3, 2, 1, 0).contiguous().view(-1).cpu().numpy()
+            I_h = np.asfortranarray(flat.reshape(tuple(img.shape), order="F"))
+            ref = orc.im2col(I_h, dict(cp, b=1))
+            got = B[:, i * per_img:(i + 1) * per_img].cpu().numpy()
+            assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), (name, i)
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 64, 25088), (4096, 256, 4096), (1000, 64, 4096)])
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_fc_gemm_vgg_shapes_fp64(m, n, k, prec):
+    """VGG-16's fc6/fc7/fc8 shapes (the timed ones): split-K over up to 9 pieces per tile,
+    against an fp64 product, with the per-output bar."""
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = (torch.rand((k, m), generator=g, device="cuda") * 2 - 1).t()
+    B = (torch.rand((n, k), generator=g, device="cuda") * 2 - 1).t()
+    C = cg.gemm(A, B, precision=prec)
+    ref = A.double() @ B.double()
+    scale = A.double().norm(dim=1).view(-1, 1) * B.double().norm(dim=0).view(1, -1)
+    err = float(((C.double() - ref).abs() / scale).max())
+    assert err <= TOL[prec], (m, n, k, prec, err)
