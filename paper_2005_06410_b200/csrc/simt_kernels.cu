@@ -80,6 +80,12 @@ struct SlabArgs {
   int32_t k_h, k_w, c_i, h_i, w_i, s, p, h_o, w_o, K;
   int32_t CB, NCB, HT, NHT, WT, NWT, HP, HPpad, WS, RB;
   int64_t ldb, plane;
+  // flat write phase (short columns: K <= ~100 rows would leave most lanes of the
+  // chunk-per-lane loop idle): one channel block, one output column per CTA, so the CTA's
+  // piece of B is one contiguous run and item = pixel * chunks + chunk indexes it directly
+  int32_t flat;
+  uint32_t nch_m, nch_p;  // item / chunks as a multiply-shift
+  uint32_t ho_m, ho_p;    // pixel / h_o likewise (several whole output columns per CTA)
 };
 
 template <int V, int NCL>
@@ -152,6 +158,25 @@ __global__ void __launch_bounds__(256) im2col_slab_kernel(const float* __restric
                       (int64_t)cb * a.RB + 4 * lane;
   const int q8 = 8 / htn, r8 = 8 - q8 * htn;
   int wl = warp / htn, hl = warp - wl * htn;
+  if (a.flat) {
+    const int items = npix * nch;
+    float* const Bcta = B + ((int64_t)h_base + (int64_t)w_base * a.h_o + (int64_t)i_b * a.h_o * a.w_o) * a.ldb;
+    for (int it = tid; it < items; it += 256) {
+      const int pix = (int)(((uint64_t)(uint32_t)it * a.nch_m) >> a.nch_p);
+      const int ch = it - pix * nch;
+      const int4 o = table4[ch];
+      // WT > 1 only with whole output columns (htn == h_o): the pixels stay one contiguous run
+      const int wl = a.WT == 1 ? 0 : (int)(((uint64_t)(uint32_t)pix * a.ho_m) >> a.ho_p);
+      const float* sp = slab_smem + (wl * a.s) * a.HPpad + (pix - wl * htn) * a.s;
+      float4 v;
+      v.x = o.x < 0 ? 0.0f : sp[o.x];
+      v.y = o.y < 0 ? 0.0f : sp[o.y];
+      v.z = o.z < 0 ? 0.0f : sp[o.z];
+      v.w = o.w < 0 ? 0.0f : sp[o.w];
+      *reinterpret_cast<float4*>(Bcta + 4 * (int64_t)it) = v;
+    }
+    return;
+  }
   if constexpr (NCL > 0) {
     // pixel-outer: the lane's chunk offsets live in registers
     int4 o[NCL];
@@ -260,8 +285,23 @@ static bool launch_im2col_slab(const float* I, float* B, int64_t ldb, const Conv
   a.K = (int32_t)g.k; a.ldb = ldb; a.plane = g.h_i * g.w_i;
   const int V = (g.h_i % 2 == 0 && reinterpret_cast<uintptr_t>(I) % 8 == 0) ? 2 : 1;
   a.HT = (int32_t)std::min<int64_t>(g.h_o, 64);
-  a.NHT = (a.h_o + a.HT - 1) / a.HT;
   a.WT = (int32_t)std::min<int64_t>(g.w_o, std::max(1, 64 / a.HT));  // ~56-64 pixels per CTA
+  // Short columns (low-channel layers: K = 27 or 147 rows): a CTA of 64 pixels would write
+  // 7-37 KB and spend its time on the fixed costs (table, fill, barrier). Take whole output
+  // columns, as many as fit 40 KB of slab, so the CTA's piece of B is one long contiguous
+  // run for the flat write phase.
+  if (g.k <= 160) {
+    const int64_t hp_full = (g.h_o - 1) * g.s + g.k_h + 2;
+    int64_t wt = 0;
+    while (wt < g.w_o && wt < 16 && g.c_i * ((wt * g.s) + g.k_w) * (hp_full + 32) * 4 <= 40 * 1024 &&
+           (wt + 1) * g.h_o <= 4096)
+      ++wt;
+    if (wt >= 1) {
+      a.HT = (int32_t)g.h_o;
+      a.WT = (int32_t)wt;
+    }
+  }
+  a.NHT = (a.h_o + a.HT - 1) / a.HT;
   a.NWT = (a.w_o + a.WT - 1) / a.WT;
   a.HP = (a.HT - 1) * a.s + a.k_h;
   a.WS = (a.WT - 1) * a.s + a.k_w;
@@ -283,6 +323,19 @@ static bool launch_im2col_slab(const float* I, float* B, int64_t ldb, const Conv
   const int64_t blocks = g.b * a.NHT * a.NWT * a.NCB;
   if (smem > 200 * 1024 || blocks > 0x7fffffffLL) return false;
   int ncl = (int)((table_rows / 4 + 31) / 32);  // chunks per lane
+  {
+    const int64_t nch = ldb / 4;
+    // < 75% of the lanes busy in the chunk-per-lane loop, and a contiguous pixel run
+    a.flat = a.NCB == 1 && (a.WT == 1 || a.HT == a.h_o) && nch * 4 < (int64_t)ncl * 32 * 3 ? 1 : 0;
+    uint32_t lh = 0;
+    while ((1ull << lh) < (uint64_t)a.h_o) ++lh;
+    a.ho_p = 31 + lh;
+    a.ho_m = (uint32_t)(((1ull << a.ho_p) + a.h_o - 1) / a.h_o);
+    uint32_t l = 0;
+    while ((1ull << l) < (uint64_t)nch) ++l;
+    a.nch_p = 31 + l;
+    a.nch_m = (uint32_t)(((1ull << a.nch_p) + nch - 1) / nch);
+  }
   if (ncl == 7) ncl = 8;
   if (ncl > 8) ncl = 0;
   *err = V == 2 ? launch_slab_v<2>(ncl, (unsigned)blocks, smem, I, B, a, st)
