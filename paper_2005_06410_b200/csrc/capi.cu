@@ -57,7 +57,7 @@ static std::mutex g_tune_mu;
 static Tuning g_tune;
 
 #define CGB_TUNING_KEYS(X)                                                                                   \
-  X(sk) X(tail) X(pair) X(cfg) X(mt) X(bn) X(tma_a) X(tma_deep) X(pstore) X(pdl) X(verbose) X(smem_pad_kb) X(tps) X(splitk) X(k2_flo) X(b_res) \
+  X(sk) X(tail) X(pair) X(cfg) X(mt) X(bn) X(tma_a) X(tma_deep) X(pstore) X(pdl) X(verbose) X(smem_pad_kb) X(tps) X(splitk) X(k2_flo) X(b_res) X(urot) \
   X(host_chunk_kb) X(host_no_bounce) X(host_copy_threads) X(debug)
 
 Tuning tuning() {
@@ -75,7 +75,7 @@ Tuning tuning() {
   env("CGB_SW_PSTORE", t.pstore); env("CGB_PDL", t.pdl); env("CGB_SW_VERBOSE", t.verbose);
   env("CGB_SW_SMEM_PAD", t.smem_pad_kb); env("CGB_HOST_CHUNK_KB", t.host_chunk_kb);
   env("CGB_HOST_NO_BOUNCE", t.host_no_bounce); env("CGB_HOST_COPY_THREADS", t.host_copy_threads);
-  env("CGB_DEBUG_SW", t.debug); env("CGB_SW_TPS", t.tps); env("CGB_SW_SPLITK", t.splitk); env("CGB_K2_FLO", t.k2_flo); env("CGB_SW_BRES", t.b_res);
+  env("CGB_DEBUG_SW", t.debug); env("CGB_SW_TPS", t.tps); env("CGB_SW_SPLITK", t.splitk); env("CGB_K2_FLO", t.k2_flo); env("CGB_SW_BRES", t.b_res); env("CGB_SW_UROT", t.urot);
 #endif
   return t;
 }

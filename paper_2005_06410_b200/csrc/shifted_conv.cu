@@ -92,6 +92,7 @@ struct Args {
   int32_t vec;        // O rows take 32-byte vector stores (k_n % 8 == 0, O 32-byte aligned)
   int32_t ksteps;     // K=8 MMA steps per tap and chunk (4; fewer in the w-im2col mode)
   int32_t tps;        // taps per filter stage group (divides B_STAGES; see the filter TMA warp)
+  int32_t urot;       // rotate the window unit -> staging warp assignment from chunk to chunk
   int32_t b_res;      // filters resident: CC*taps <= B_STAGES and one filter tile, so stage cc*taps+tap is
                       // loaded once per CTA and never recycled (no per-tile filter hand-overs)
   int32_t pstore;     // epilogue stores: 1 lane pairs 64 B (default), 0 per-lane 32 B (CGB_SW_PSTORE=0)
@@ -238,12 +239,12 @@ CGB_DEV void issue_tap(uint32_t d_base, uint64_t at, uint64_t at_lo, uint64_t bt
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const uint64_t ad = at + (uint64_t)(mt * 1024) + (uint64_t)kk * a_kstep;
-        const uint64_t bd = bt + (uint64_t)(hf * (UN / 32) * 256 + kk * 64);
+        const uint64_t bd = bt + (uint64_t)(hf * ((PAIR ? UN / 2 : UN) / 32) * 256 + kk * 64);
         const uint32_t d = d_base + (uint32_t)(mt * BN + hf * UN);
         const uint32_t acc = kk == 0 ? first : 1u;
         if (SPLIT) {
           const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024) + (uint64_t)kk * a_kstep;
-          const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (UN / 32) * 256 + kk * 64);
+          const uint64_t bd_lo = bt_lo + (uint64_t)(hf * ((PAIR ? UN / 2 : UN) / 32) * 256 + kk * 64);
           if (PAIR) {
             mma_tf32_2cta(d, ad_lo, bd, idesc, acc);
             mma_tf32_2cta(d, ad, bd_lo, idesc, 1);
@@ -272,12 +273,12 @@ CGB_DEV void issue_tap_partial(uint32_t d_base, uint64_t at, uint64_t at_lo, uin
 #pragma unroll 1
       for (int mt = 0; mt < mtc; ++mt) {
         const uint64_t ad = at + (uint64_t)(mt * 1024) + (uint64_t)kk * a_kstep;
-        const uint64_t bd = bt + (uint64_t)(hf * (UN / 32) * 256 + kk * 64);
+        const uint64_t bd = bt + (uint64_t)(hf * ((PAIR ? UN / 2 : UN) / 32) * 256 + kk * 64);
         const uint32_t d = d_base + (uint32_t)(mt * BN + hf * UN);
         const uint32_t acc = kk == 0 ? first : 1u;
         if (SPLIT) {
           const uint64_t ad_lo = at_lo + (uint64_t)(mt * 1024) + (uint64_t)kk * a_kstep;
-          const uint64_t bd_lo = bt_lo + (uint64_t)(hf * (UN / 32) * 256 + kk * 64);
+          const uint64_t bd_lo = bt_lo + (uint64_t)(hf * ((PAIR ? UN / 2 : UN) / 32) * 256 + kk * 64);
           if (PAIR) {
             mma_tf32_2cta(d, ad_lo, bd, idesc, acc);
             mma_tf32_2cta(d, ad, bd_lo, idesc, 1);
@@ -682,6 +683,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
     // (from-scratch lookup here: these producers are the register-tightest path, and their
     // tiles carry whole chunks of staging work)
+    int urot = 0;  // rotation of the unit -> warp assignment (units staged so far, mod the warps)
     for (int j = 0; seg_get(a, gid, j, tile, cc0, cc1); ++j) {
       int32_t m0;
       int mtc;
@@ -697,8 +699,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t base_hi = smem_u32(a_slot(s, 0));
         const uint32_t base_lo = smem_u32(a_slot(s, SPLIT ? 1 : 0));
         const int cmax = a.c_i - cc * BK;
-        // UPI units in flight per iteration (UPI x 32 loads per thread)
-        for (int u = warp; u < units && !CGB_DBG(1); u += UPI * PRODUCER_WARPS) {
+        // UPI units in flight per iteration (UPI x 32 loads per thread). The unit -> warp
+        // assignment rotates from chunk to chunk (unit u of this chunk goes to warp
+        // (u + rot) % 12): with 18 or 20 units per chunk the same warps would otherwise
+        // always carry the extra unit, and with fewer units than warps (1x1 layers: 4 or
+        // 8 rows blocks per chunk) the same warps would always idle while the deep A ring
+        // lets different warps fill different chunks at once.
+        const int ufirst = a.urot ? (warp + PRODUCER_WARPS - urot) % PRODUCER_WARPS : warp;
+        if (a.urot) urot = (urot + units) % PRODUCER_WARPS;
+        for (int u = ufirst; u < units && !CGB_DBG(1); u += UPI * PRODUCER_WARPS) {
           float v[UPI][BK];
           int32_t row[UPI];
           uint32_t off[UPI];
@@ -767,10 +776,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       };
       const uint32_t b0_hi = smem_u32(b_slot(0, 0)), b0_lo = smem_u32(b_slot(0, SPLIT ? 1 : 0));
+      // Filter column of this CTA's j-th 32-filter block. A pair UMMA of N = UMMA_N takes
+      // UMMA_N / 2 filters from each CTA, so for BN > 256 (two UMMAs per k-step) the CTA's
+      // blocks interleave the two N halves: accumulator column c stays filter n0 + c.
+      constexpr int HB = (PAIR ? C::UMMA_N / 2 : C::UMMA_N) / 32;  // blocks per UMMA half in this CTA
+      auto fcol = [&](int nt0, int j) {
+        return nt0 + (j / HB) * C::UMMA_N + (PAIR ? (int)rank * (C::UMMA_N / 2) : 0) + 32 * (j % HB);
+      };
       int tile, cc0, cc1;
       if (a.b_res) {
         // resident filters: every (chunk, tap) stage once, each on its own barrier (phase 0)
-        const int n0 = (int)rank * C::NB;
+        const int n0 = 0;
         for (int cc = 0; cc < a.CC; ++cc)
           for (int tap = 0; tap < a.taps; ++tap) {
             const int st_i = cc * a.taps + tap;
@@ -779,13 +795,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int j = 0; j < C::NB / 32; ++j) {
               if (PAIR) {
-                tma_load_3d_2sm(b0_hi + stage_off + j * 4096, &tmap_hi, lead_b_full + st_i * 8, n0 + 32 * j, tap, cc * BK);
+                tma_load_3d_2sm(b0_hi + stage_off + j * 4096, &tmap_hi, lead_b_full + st_i * 8, fcol(n0, j), tap, cc * BK);
                 if (SPLIT)
-                  tma_load_3d_2sm(b0_lo + stage_off + j * 4096, &tmap_lo, lead_b_full + st_i * 8, n0 + 32 * j, tap,
+                  tma_load_3d_2sm(b0_lo + stage_off + j * 4096, &tmap_lo, lead_b_full + st_i * 8, fcol(n0, j), tap,
                                   cc * BK);
               } else {
-                tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[st_i], n0 + 32 * j, tap, cc * BK);
-                if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[st_i], n0 + 32 * j, tap, cc * BK);
+                tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[st_i], fcol(n0, j), tap, cc * BK);
+                if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[st_i], fcol(n0, j), tap, cc * BK);
               }
             }
           }
@@ -793,7 +809,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int ait = 0;  // TMA-fed A: chunk counter (window slot ring)
       const Seg sg4 = seg_init(a, gid);
       for (int j = 0; seg_at(a, sg4, gid, j, tile, cc0, cc1); ++j) {
-        const int n0 = (tile / a.m_tiles) * BN + (int)rank * C::NB;
+        const int n0 = (tile / a.m_tiles) * BN;
         int32_t am0 = 0;
         int amtc = 0;
         if (a.tma_a) tile_rows<MT, PAIR>(a, tile, rank, am0, amtc);
@@ -832,14 +848,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int j = 0; j < C::NB / 32; ++j) {
                 if (PAIR) {
-                  tma_load_3d_2sm(b0_hi + stage_off + j * 4096, &tmap_hi, lead_b_full + gb * 8, n0 + 32 * j, tap,
+                  tma_load_3d_2sm(b0_hi + stage_off + j * 4096, &tmap_hi, lead_b_full + gb * 8, fcol(n0, j), tap,
                                   cc * BK);
                   if (SPLIT)
-                    tma_load_3d_2sm(b0_lo + stage_off + j * 4096, &tmap_lo, lead_b_full + gb * 8, n0 + 32 * j, tap,
+                    tma_load_3d_2sm(b0_lo + stage_off + j * 4096, &tmap_lo, lead_b_full + gb * 8, fcol(n0, j), tap,
                                     cc * BK);
                 } else {
-                  tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[gb], n0 + 32 * j, tap, cc * BK);
-                  if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[gb], n0 + 32 * j, tap, cc * BK);
+                  tma_load_3d(b0_hi + stage_off + j * 4096, &tmap_hi, &b_full[gb], fcol(n0, j), tap, cc * BK);
+                  if (SPLIT) tma_load_3d(b0_lo + stage_off + j * 4096, &tmap_lo, &b_full[gb], fcol(n0, j), tap, cc * BK);
                 }
               }
             }
@@ -1199,6 +1215,14 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   // Filters resident in the ring (no recycling, no per-tile hand-overs): when every
   // (chunk, tap) stage of the one filter tile fits -- the w-im2col layers (stem: 7 taps,
   // VGG conv1: 3), short 1x1 layers.
+  {
+    // rotation only where a chunk has fewer units than staging warps (the staged 1x1 layers:
+    // 7x7 2048->512 97 -> 80 us, 512->2048 82 -> 73 us); with 18-20 units per chunk (3x3
+    // windows) it measured neutral to slightly worse (s2 56->28: 94.7 vs 93.1 us)
+    const int rpu = 32 / a.nph_h;
+    const int units = a.nph_w * ((a.R + rpu - 1) / rpu);
+    a.urot = tu.urot != 0 && units < PRODUCER_WARPS;
+  }
   a.b_res = tu.b_res != 0 && a.CC * a.taps <= B_STAGES && a.n_tiles == 1 && !(tu.debug & 8);
   size_t smem = base_smem;
   if (tu.smem_pad_kb > 0)  // profiling: shrink the L1 carve-out
@@ -1473,6 +1497,9 @@ static const Cand kCands[] = {
     // probes (tuning cfg only)
     {1, 128, 0, 2, 6, 1, 2}, {1, 256, 0, 2, 3, 1, 2}, {1, 256, 0, 2, 4, 1, 2},
     {2, 64, 0, 2, 8, 0, 1},  // single CTA with a ring that holds the stem's 7 taps resident
+    // BN = 512 (two N = 256 UMMAs per k-step, all of TMEM for one 128-row subtile per CTA):
+    // staging-bound 1x1 layers with k_n >= 512 stage each window once instead of twice
+    {1, 512, 0, 4, 4, 1, 1}, {1, 512, 0, 2, 4, 1, 1},
 };
 constexpr int kNumCands = sizeof(kCands) / sizeof(kCands[0]);
 constexpr int kFirstDeepCand = 36;
@@ -1481,6 +1508,7 @@ constexpr int kFirstSplit2Cand = 43;  // 3xTF32 with two window slots
 constexpr int kFirstTmaACand = 48;   // deep A rings, tried first for 1x1 layers
 constexpr int kFirstProbeCand = 50;  // candidates from here on are CGB_SW_CFG probes only
 constexpr int kWimCand = 53;         // the w-im2col layers' single-CTA kernel (dispatch)
+constexpr int kBn512Cand = 54;       // staged 1x1 layers with k_n in (256, 512]: one 512-filter tile (dispatch)
 
 static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& tl, const float* I, float* O,
                                const Args& a, cudaStream_t st, const Tuning& tu) {
@@ -1541,6 +1569,8 @@ static cudaError_t launch_cand(int i, const CUtensorMap& th, const CUtensorMap& 
     CGB_SW_CASE(51, 1, 256, false, 2, 3, true, 2)
     CGB_SW_CASE(52, 1, 256, false, 2, 4, true, 2)
     CGB_SW_CASE(53, 2, 64, false, 2, 8, false, 1)
+    CGB_SW_CASE(54, 1, 512, false, 4, 4, true, 1)
+    CGB_SW_CASE(55, 1, 512, false, 2, 4, true, 1)
     default: return cudaErrorNotSupported;
   }
 #undef CGB_SW_CASE
@@ -1552,12 +1582,25 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
                             bool split, int sms, cudaStream_t st) {
   const Tuning tu = tuning();
   int bn = bn_for(a.k_n);
-  if (tu.bn == 64 || tu.bn == 128 || tu.bn == 256) bn = tu.bn;  // forced filter tile
+  if (tu.bn == 64 || tu.bn == 128 || tu.bn == 256 || tu.bn == 512) bn = tu.bn;  // forced filter tile
   const int n_tiles = (a.k_n + bn - 1) / bn;
   if (tu.cfg >= 0) {  // forced candidate (when it matches the filter tile and precision)
     const int i = tu.cfg;
     if (i < kNumCands && kCands[i].bn == bn && kCands[i].split == (int)split)
       return launch_cand(i, th, tl, I, O, a, st, tu);
+  }
+  // Staged 1x1 layers with 256 < k_n <= 512 and a long contraction (7x7 2048->512): one
+  // 512-filter tile stages every window once instead of twice (79.4 -> 71.2 us; not for
+  // k_n = 2048, where four 512-tiles per pixel tile measured slower: 81 vs 73 us).
+  // Only with at least half a round of 256-row pair tiles: fewer tiles go to split-K, whose
+  // piece counts (and rounding) would then depend on the filter tile.
+  if (a.taps == 1 && !a.tma_a && !a.wim && !split && a.k_n > 256 && a.k_n <= 512 && a.CC >= 16 && tu.bn == 0 &&
+      (a.Mp + 255) / 256 >= sms / 4) {
+    cudaError_t e = launch_cand(kBn512Cand, th, tl, I, O, a, st, tu);
+    if (e != cudaErrorNotSupported) {
+      if (tu.verbose) fprintf(stderr, "[cgb] shifted cand %d (1x1, BN = 512)\n", kBn512Cand);
+      return e;
+    }
   }
   // w-im2col layers (one chunk of k_h taps per tile: ~1 us of UMMAs between hand-overs):
   // single CTAs -- CTA-scope barriers instead of the pair's cluster-scope hand-overs --

@@ -641,3 +641,49 @@ def test_resident_filters_bitwise(orc, cp, prec):
                 outs[(pair, br)] = to_host(cg.conv(Fd, Id, cp, precision=prec))
             assert per_output_error(outs[(pair, br)], ref, scale) <= TOL[prec], (pair, br)
         assert np.array_equal(outs[(pair, 0)].view(np.uint32), outs[(pair, 1)].view(np.uint32)), pair
+
+
+# ---------------------------------------------------------------- BN = 512 filter tiles
+@pytest.mark.parametrize("cp", [
+    dict(k_n=512, k_h=1, k_w=1, c_i=128, h_i=7, w_i=7, b=9, s=1, p=0),     # the 1x1 7x7 layers it is for
+    dict(k_n=1024, k_h=1, k_w=1, c_i=96, h_i=7, w_i=7, b=20, s=1, p=0),    # two filter tiles
+    dict(k_n=640, k_h=1, k_w=1, c_i=64, h_i=14, w_i=14, b=3, s=1, p=0),    # ragged second tile, TMA-fed A
+    dict(k_n=512, k_h=3, k_w=3, c_i=32, h_i=9, w_i=9, b=4, s=1, p=1),      # 3x3 windows
+])
+def test_bn512_tiles_bitwise(orc, cp):
+    """Filter tiles of 512 (two N = 256 UMMAs per k-step; each CTA of a pair holds the two
+    N halves interleaved): every output accumulates the same products in the same order as
+    with 256-filter tiles, so the results are bitwise equal, and within the bar of the oracle."""
+    F, I = rand_inputs(cp, 5120)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    Fd, Id = to_dev(F), to_dev(I)
+    with cg.tuning(bn=256):
+        base = to_host(cg.conv(Fd, Id, cp, precision="tf32"))
+    assert per_output_error(base, ref, scale) <= TOL["tf32"]
+    for cfg in (54, 55):
+        with cg.tuning(bn=512, cfg=cfg, verbose=0):
+            out = to_host(cg.conv(Fd, Id, cp, precision="tf32"))
+        assert cg.last_path() == "tcgen05-shifted"
+        assert np.array_equal(out.view(np.uint32), base.view(np.uint32)), cfg
+
+
+def test_bn512_dispatch_and_unit_rotation(orc):
+    """A staged 1x1 layer with a long contraction and k_n = 512 takes the 512-filter tile by
+    itself, and its window units rotate over the staging warps from chunk to chunk: both
+    are pure scheduling, bitwise equal to the 256-filter tiles without rotation."""
+    cp = dict(k_n=512, k_h=1, k_w=1, c_i=544, h_i=7, w_i=7, b=200, s=1, p=0)  # 9800 rows: 39 pair tiles
+    F, I = rand_inputs(cp, 5121)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    Fd, Id = to_dev(F), to_dev(I)
+    with cg.tuning(bn=256, urot=0):
+        base = to_host(cg.conv(Fd, Id, cp, precision="tf32"))
+    assert per_output_error(base, ref, scale) <= TOL["tf32"]
+    for urot in (0, 1):
+        with cg.tuning(urot=urot):
+            out = to_host(cg.conv(Fd, Id, cp, precision="tf32"))
+        assert np.array_equal(out.view(np.uint32), base.view(np.uint32)), urot
+    with cg.tuning(bn=256, urot=1):
+        out = to_host(cg.conv(Fd, Id, cp, precision="3xtf32"))
+    assert per_output_error(out, ref, scale) <= TOL["3xtf32"]
