@@ -1216,12 +1216,12 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   // (chunk, tap) stage of the one filter tile fits -- the w-im2col layers (stem: 7 taps,
   // VGG conv1: 3), short 1x1 layers.
   {
-    // rotation only where a chunk has fewer units than staging warps (the staged 1x1 layers:
+    // rotation only where a chunk has fewer units than staging warps and one tap (the staged 1x1 layers:
     // 7x7 2048->512 97 -> 80 us, 512->2048 82 -> 73 us); with 18-20 units per chunk (3x3
     // windows) it measured neutral to slightly worse (s2 56->28: 94.7 vs 93.1 us)
     const int rpu = 32 / a.nph_h;
     const int units = a.nph_w * ((a.R + rpu - 1) / rpu);
-    a.urot = tu.urot != 0 && units < PRODUCER_WARPS;
+    a.urot = tu.urot != 0 && units < PRODUCER_WARPS && a.taps == 1;  // (3x3 MT = 1 tiles, 5 units: 1.5% slower)
   }
   a.b_res = tu.b_res != 0 && a.CC * a.taps <= B_STAGES && a.n_tiles == 1 && !(tu.debug & 8);
   size_t smem = base_smem;
