@@ -88,6 +88,10 @@ cgb_status cgb_validate_blocking(const cgb_blocking_params* bp);
  * additionally holds B-hat (k x n). Pass workspace=NULL to cgb_conv* to let the
  * library use its own tracked, cached device allocation. */
 int64_t cgb_conv_workspace_bytes(int algo, int precision, const cgb_conv_params* cp);
+/* The same for cgb_gemm (C m x n = A m x k * B k x n, aligned B): the filter hi/lo split
+ * of A for 3xTF32 when A is small; none in TF32 mode, and none for large A (> 8 MB: fc
+ * weights), whose lo tile is split inside the kernel. -1 on bad dimensions. */
+int64_t cgb_gemm_workspace_bytes(int precision, int64_t m, int64_t n, int64_t k);
 
 /* ---- device-pointer entry points (asynchronous on `stream`) ---- */
 cgb_status cgb_conv(int algo, int precision, const float* F, const float* I,

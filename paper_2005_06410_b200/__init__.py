@@ -32,7 +32,7 @@ __all__ = [
     "im2col", "im2col_workspace_bytes", "output_dims", "scratch_peak_bytes", "scratch_reset_peak",
     "scratch_set_limit", "kernel_launch_count", "last_path", "PRECISIONS", "ALGOS", "gemm", "conv_direct",
     "set_tuning", "get_tuning", "tuning",
-    "IoError", "conv_workspace_bytes", "LayerSpec", "ModelSpec", "LayerResult", "ParseError", "UnknownLayerKind", "parse_model",
+    "IoError", "conv_workspace_bytes", "gemm_workspace_bytes", "LayerSpec", "ModelSpec", "LayerResult", "ParseError", "UnknownLayerKind", "parse_model",
     "model_workspace_bytes", "run_inference", "write_csv",
 ]
 
@@ -142,11 +142,14 @@ def convgemm_scratch_bytes(blocking: BlockingParams | None = None) -> int:
     return (bp.mc * bp.kc + bp.kc * bp.nc) * 4
 
 
-def conv_workspace_bytes(cp, algo: str = "fused", precision: str = "auto", external_b: bool = False) -> int:
-    """Device workspace one call takes (filter split + B-hat for the explicit path);
-    ``external_b``: B-hat is the caller's (``gemm``), so only the filter part counts."""
-    a = ALGOS["fused"] if external_b else ALGOS[algo]  # same filter part, no B-hat
-    return lib.cgb_conv_workspace_bytes(a, PRECISIONS[precision], ctypes.byref(ConvParams.of(cp).c()))
+def conv_workspace_bytes(cp, algo: str = "fused", precision: str = "auto") -> int:
+    """Device workspace one call takes (filter split + B-hat for the explicit path)."""
+    return lib.cgb_conv_workspace_bytes(ALGOS[algo], PRECISIONS[precision], ctypes.byref(ConvParams.of(cp).c()))
+
+
+def gemm_workspace_bytes(m: int, n: int, k: int, precision: str = "auto") -> int:
+    """Device workspace one ``gemm`` call takes (cgb_gemm_workspace_bytes)."""
+    return lib.cgb_gemm_workspace_bytes(PRECISIONS[precision], m, n, k)
 
 
 def scratch_peak_bytes() -> int:

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("CGB_LIB_OVERRIDE") or os.path.join(HERE, "libconvgemm
 # exported symbols, in include/convgemm_b200.h order
 SYMBOLS = (
     "cgb_output_dims", "cgb_gemm_dims", "cgb_im2col_workspace_bytes", "cgb_validate_blocking",
-    "cgb_conv_workspace_bytes", "cgb_conv", "cgb_conv_gemm", "cgb_conv_im2col_gemm", "cgb_im2col",
+    "cgb_conv_workspace_bytes", "cgb_gemm_workspace_bytes", "cgb_conv", "cgb_conv_gemm", "cgb_conv_im2col_gemm", "cgb_im2col",
     "cgb_gemm", "cgb_conv_host", "cgb_scratch_current_bytes", "cgb_scratch_peak_bytes", "cgb_scratch_reset_peak",
     "cgb_scratch_set_limit", "cgb_scratch_release", "cgb_last_error", "cgb_version",
     "cgb_kernel_launch_count", "cgb_last_path", "cgb_debug_sw_stats", "cgb_set_tuning", "cgb_get_tuning",
@@ -50,6 +50,7 @@ def _load() -> ctypes.CDLL:
         "cgb_im2col_workspace_bytes": (i64, [cpp]),
         "cgb_validate_blocking": (st, [bpp]),
         "cgb_conv_workspace_bytes": (i64, [ctypes.c_int, ctypes.c_int, cpp]),
+        "cgb_gemm_workspace_bytes": (i64, [ctypes.c_int, i64, i64, i64]),
         "cgb_conv": (st, [ctypes.c_int, ctypes.c_int, vp, vp, cpp, vp, vp, ctypes.c_size_t, vp]),
         "cgb_conv_gemm": (st, [vp, vp, cpp, bpp, ctypes.c_int, vp, ctypes.c_int, vp]),
         "cgb_conv_im2col_gemm": (st, [vp, vp, cpp, bpp, ctypes.c_int, vp, ctypes.c_int, vp]),

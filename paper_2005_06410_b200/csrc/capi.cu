@@ -357,6 +357,14 @@ int64_t cgb_conv_workspace_bytes(int algo, int precision, const cgb_conv_params*
   return std::max<int64_t>(pl.f_bytes + pl.b_bytes, use_wim(algo, prec, g) ? wim_filter_bytes(prec, g) : 0);
 }
 
+int64_t cgb_gemm_workspace_bytes(int precision, int64_t m, int64_t n, int64_t k) {
+  if (m < 1 || n < 1 || k < 1) return -1;
+  cgb_conv_params cp{m, 1, 1, k, 1, 1, n, 1, 0};  // as cgb_gemm: a 1x1 conv over 1x1 images
+  ConvGeom g;
+  if (make_geom(&cp, &g)) return -1;
+  return make_plan(CGB_ALGO_EXPLICIT, resolve_precision(precision, g), g, nullptr).f_bytes;  // B is the caller's
+}
+
 // The operator body behind cgb_conv and cgb_gemm. Bext != NULL: the lowered matrix B
 // (k x n, leading dimension ldb_ext) is the caller's (gemm over a MatrixSource,
 // gemm.hpp:100-105): the explicit path without the im2col step or its workspace.

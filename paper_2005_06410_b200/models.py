@@ -9,7 +9,13 @@ per conv / fc / pool, conv geometry at batch 1).
   the block's first 1x1 conv (v1), and a projection shortcut (1x1, same stride) follows
   the three convs of the first block of every stage; fc 1000.
 
-Either can be written out as model text (``ModelSpec.to_text``) and parsed back.
+* ``alexnet()`` -- the five convolutions of the single-tower AlexNet (11x11/s4, 5x5, three
+  3x3; widths 64, 192, 384, 384, 256), pools to 26, 13 and 6, fc 4096, 4096, 1000. The
+  reference's file lists every conv unpadded and with the input extents 224, 55, 27, 13,
+  13 (each line is an independent layer geometry, not a shape-propagated chain); the
+  same table is kept here so the sweep times the same GEMMs (m x n x k) as the reference.
+
+All can be written out as model text (``ModelSpec.to_text``) and parsed back.
 """
 from __future__ import annotations
 
@@ -56,4 +62,22 @@ def resnet50() -> ModelSpec:
     return m
 
 
-MODELS = {"vgg16": vgg16, "resnet50": resnet50}
+def alexnet() -> ModelSpec:
+    m = ModelSpec("alexnet")
+    # (filters, kernel, stride, input extent) per conv; a pool (output extent) follows where given
+    table = ((64, 11, 4, 224, 26), (192, 5, 1, 55, 13), (384, 3, 1, 27, None), (384, 3, 1, 13, None),
+             (256, 3, 1, 13, 6))
+    c = 3
+    for width, k, s, h, pool in table:
+        m.layers.append(_conv(width, k, c, h, s, 0))
+        c = width
+        if pool:
+            m.layers.append(LayerSpec("pool", pool_h=pool, pool_w=pool, pool_c=c))
+    k = 6 * 6 * c
+    for out in (4096, 4096, 1000):
+        m.layers.append(LayerSpec("fc", fc_m=out, fc_k=k))
+        k = out
+    return m
+
+
+MODELS = {"alexnet": alexnet, "vgg16": vgg16, "resnet50": resnet50}

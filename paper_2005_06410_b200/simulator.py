@@ -211,7 +211,7 @@ def run_inference(model: ModelSpec, batch: int, algo: str = "convgemm", threads:
     size); the device tiling is internal."""
     import torch
 
-    from . import (InvalidGeometry, _validate_blocking, conv, conv_workspace_bytes, gemm, gemm_dims, im2col,
+    from . import (InvalidGeometry, _validate_blocking, conv, conv_workspace_bytes, gemm, gemm_dims, gemm_workspace_bytes, im2col,
                    output_dims)
     if batch < 1:
         raise InvalidGeometry("batch must be positive")
@@ -238,7 +238,7 @@ def run_inference(model: ModelSpec, batch: int, algo: str = "convgemm", threads:
             W, X, Y = _view2(weights, m, k), _view2(src, k, n), _view2(dst, m, n)
             prec = precision  # fc layers are gemm under every algo (bench.cpp:140-153)
             op = lambda W=W, X=X, Y=Y, prec=prec: gemm(W, X, precision=prec, out=Y)  # noqa: E731
-            ws = conv_workspace_bytes(_fc_params(layer, batch), "explicit", prec, external_b=True)
+            ws = gemm_workspace_bytes(m, n, k, prec)
         else:
             cp = _with_batch(layer.conv, batch)
             h_o, w_o = output_dims(cp)
@@ -308,11 +308,6 @@ def _per_output_error(conv, F, I, O, ref, cp):
     bn = conv(ones, sq, c4, "fused", "ffma")[0].clamp_min(0).sqrt()  # (h_o, w_o, b)
     scale = (fn.view(-1, 1, 1, 1) * bn.unsqueeze(0)).clamp_min(1e-30)
     return float(((O - ref).abs() / scale).max())
-
-
-def _fc_params(layer, batch):
-    from . import ConvParams
-    return ConvParams(layer.fc_m, 1, 1, layer.fc_k, 1, 1, batch, 1, 0)
 
 
 def write_csv(out, model: ModelSpec, batch: int, algo: str, threads: int, results: list, header: bool = True):

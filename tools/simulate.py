@@ -13,7 +13,7 @@ import paper_2005_06410_b200 as cg  # noqa: E402
 from paper_2005_06410_b200 import models  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--models", default="vgg16,resnet50")
+ap.add_argument("--models", default="alexnet,vgg16,resnet50")
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--algo", default="convgemm")
 ap.add_argument("--precision", default="tf32")
