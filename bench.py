@@ -576,7 +576,13 @@ def run_gpu_arm(args, world, rank, local):
     # supplementary: independent layers issued on forked streams (never the headline)
     concurrent = {}
     for ns in [int(x) for x in args.concurrent.split(",") if x]:
-        ms = time_concurrent(cg, torch, tensors, headline, args.steps, args.warmup, flush, world, ns)
+        try:
+            ms = time_concurrent(cg, torch, tensors, headline, args.steps, args.warmup, flush, world, ns)
+        except Exception as ex:  # noqa: BLE001  (supplementary leg: never takes the contract line down)
+            if world > 1:
+                raise
+            concurrent[str(ns)] = {"streams": ns, "error": f"{type(ex).__name__}: {ex}"[:200]}
+            continue
         ms_c = max_over_ranks(statistics.mean(ms), world)
         ach = step_flops_local / (ms_c * 1e-3) / 1e12
         concurrent[str(ns)] = {"streams": ns, "ms_per_step": ms_c, "value": total_flops / (ms_c * 1e-3) / 1e9,

@@ -10,7 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import _prof  # noqa: E402,F401  (profiling build: CGB_* env knobs)
 import paper_2005_06410_b200 as cg
 import bench
-tensors = bench.make_layer_tensors(cg, torch, bench.LAYERS, 128, 0, 1)
+BATCH_TL = int(os.environ.get("TL_BATCH", "128"))
+tensors = bench.make_layer_tensors(cg, torch, bench.LAYERS, BATCH_TL, 0, 1)
 def step():
     for layer, cp, F, I, O in tensors:
         cg.conv(F, I, cp, algo="fused", precision="tf32", out=O)
