@@ -273,6 +273,20 @@ def run_reference_arm(args, world, rank):
         step_t.append(time.perf_counter() - t0)
     step_flops = sum(flops(cp) for _, cp, _, _ in data)
     value = step_flops / statistics.mean(step_t) / 1e9
+    # supplementary (SURVEY 8(d) times both CPU operators): the reference's explicit
+    # conv_im2col_gemm<float>, one pass over the 7 layers at a b=8 sample
+    explicit = None
+    if kind == "reference" and not args.quick:
+        from oracle.oracle import Reference
+        ref = Reference()
+        small = host_tensors(LAYERS, min(8, sample_b))
+        t0 = time.perf_counter()
+        for layer, cp, F, I in small:
+            ref.conv_im2col_gemm(F, I, cp, threads=threads)
+        dt = time.perf_counter() - t0
+        explicit = {"value": sum(flops(cp) for _, cp, _, _ in small) / dt / 1e9, "unit": UNIT,
+                    "algo": "conv_im2col_gemm (reference explicit im2col + gemm)",
+                    "sample": f"one pass over the 7 layers at b={min(8, sample_b)}, threads={threads}"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(step_t),
@@ -285,6 +299,7 @@ def run_reference_arm(args, world, rank):
                          "sample": f"each step = the 7 layers at b={sample_b} (of {BATCH}), "
                                    f"{step_flops / 1e9:.1f} GFLOP, conv_gemm<float> threads={threads}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "explicit": explicit,
     }
     print(json.dumps(line), flush=True)
     return 0
