@@ -97,7 +97,8 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             m = json.load(f)
-        p = {"hbm_gbs": float(m["hbm_gbs"]), "bf16_tflops": float(m["bf16_tflops"]), "src": "MEASURED_PEAKS.json"}
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "bf16_tflops": float(m["bf16_tflops"]), "src": "MEASURED_PEAKS.json",
+             "bf16_sustained": float(m.get("bf16_tflops_sustained") or 0) or None}
     except Exception:  # noqa: BLE001
         pass
     p["tf32_tflops"] = p["bf16_tflops"] / 2.0
@@ -646,6 +647,9 @@ def run_gpu_arm(args, world, rank, local):
                      "unit": "TFLOP/s", "frac": hm["achieved_tflops"] / peak, "traffic": traffic,
                      "peak_src": pk["tf32_src"],
                      "frac_vs_other_peaks": {
+                         "MEASURED_PEAKS bf16_tflops_sustained/2 (the back-to-back figure; context only, `peak` is "
+                         "the larger burst figure)":
+                             hm["achieved_tflops"] / (pk["bf16_sustained"] / 2) if pk.get("bf16_sustained") else None,
                          "cuBLAS TF32 8192^3 burst on this pool (profiles/tf32_peak.json)":
                              hm["achieved_tflops"] / pk["cublas_tf32"] if pk.get("cublas_tf32") else None,
                          "tcgen05 kind::tf32 UMMA microbenchmark 1190 @1965 MHz (tools/umma_bench.cu, pair_bench.cu)":
