@@ -6,6 +6,11 @@
   stem      the 7x7/s2 stem at b=256 (w-im2col mode of the shifted-window kernel)
   pw56      1x1 56^2 64->256 at b=256 (TMA-fed A)
   direct    conv_direct (bit-exact reference order) on a small layer
+  gather    AlexNet conv1 (11x11 stride 4, 3->64, 224^2) at b=64: outside the shifted-window
+            domain (stride > 2), the tap-major gather kernel or the reference-order implicit GEMM
+  tgather   3x3 stride 3, 64->128, 56^2, b=64: c_i >= 16 outside the shifted-window domain -> the
+            tap-major gather kernel (tc_gather)
+  alex5     AlexNet conv2 (5x5, 64->192, 55^2, unpadded) at b=64 on the shifted-window kernel (25 taps)
 Runs the operation twice (the first launch warms allocations); profile with -s/-c."""
 import os
 import sys
@@ -49,6 +54,11 @@ for _ in range(2):
         cg.conv(F, I, cp, precision="tf32")
     elif case == "pw56":
         cp, F, I = layer("pw_56_64_256")
+        cg.conv(F, I, cp, precision="tf32")
+    elif case in ("gather", "alex5", "tgather"):
+        cp = dict(k_n=128, k_h=3, k_w=3, c_i=64, h_i=56, w_i=56, b=64, s=3, p=1) if case == "tgather" else dict(k_n=64, k_h=11, k_w=11, c_i=3, h_i=224, w_i=224, b=64, s=4, p=0) if case == "gather" else \
+            dict(k_n=192, k_h=5, k_w=5, c_i=64, h_i=55, w_i=55, b=64, s=1, p=0)
+        F, I = configs.make_tensors(torch, cg.empty_tensor4, cp, "uniform", 11)
         cg.conv(F, I, cp, precision="tf32")
     elif case == "direct":
         cp, F, I = layer("r50_3x3_14_256", b=2)
