@@ -538,6 +538,54 @@ def test_workspace_per_stream_concurrent(orc):
             assert per_output_error(to_host(o[k]), ref, orc.output_scale(F, I, cp)) <= 1e-5
 
 
+def test_forked_streams_graph_bitwise_equal_to_serial(orc):
+    """Independent layers issued on forked streams inside one captured graph (bench.py's
+    supplementary `concurrent` step): stream-K layers (per-stream tile counters), a split-K
+    layer (per-stream partial-tile workspace) and a whole-tile layer running concurrently
+    give the bits of the serial launches, replay after replay."""
+    cases = [dict(SK_CASES[0]), dict(SK_CASES[1]),
+             dict(k_n=256, k_h=3, k_w=3, c_i=256, h_i=14, w_i=14, b=4, s=1, p=1),   # few tiles: split-K
+             dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=56, w_i=56, b=6, s=1, p=1)]
+    ins = []
+    for i, cp in enumerate(cases):
+        F, I = rand_inputs(cp, 900 + i)
+        ins.append((cp, to_dev(F), to_dev(I)))
+    serial = [cg.conv(dF, dI, cp, algo="fused", precision="tf32").clone() for cp, dF, dI in ins]
+    torch.cuda.synchronize()
+    outs = [torch.zeros_like(o) for o in serial]
+    side = [torch.cuda.Stream() for _ in range(2)]
+
+    def step():
+        cur = torch.cuda.current_stream()
+        for st in side:
+            st.wait_stream(cur)
+        for i, (cp, dF, dI) in enumerate(ins):
+            with torch.cuda.stream(side[i % 2]):
+                cg.conv(dF, dI, cp, algo="fused", precision="tf32", out=outs[i])
+        for st in side:
+            cur.wait_stream(st)
+
+    warm = torch.cuda.Stream()
+    warm.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(warm):
+        step()  # allocates the per-stream counters / workspaces outside the capture
+    torch.cuda.current_stream().wait_stream(warm)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for rep in range(5):
+        for o in outs:
+            o.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for i, (o, ref) in enumerate(zip(outs, serial)):
+            assert torch.equal(o, ref), (rep, cases[i])
+    cp, dF, dI = ins[0]
+    F, I = rand_inputs(cp, 900)
+    assert per_output_error(to_host(outs[0]), orc.conv_gemm(F, I, cp), orc.output_scale(F, I, cp)) <= TOL["tf32"]
+
+
 def test_workspace_growth_keeps_captured_buffer(orc):
     """A graph captured with the cached workspace keeps working after a later call on the
     same stream needs (and allocates) a bigger one: captured buffers are never freed."""
