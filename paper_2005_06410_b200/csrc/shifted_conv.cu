@@ -1440,7 +1440,12 @@ static Args make_args(const ConvGeom& g) {
 }  // namespace sw
 
 // Domain: filters through the tap-major TMA map (k_n % 4 == 0), at least half a channel
-// chunk, stride <= 2 (<= 4 phase planes), and a padded plane that wastes < 70% rows.
+// chunk, stride <= 2 (<= 4 phase planes). The padded plane may hold many more rows than
+// outputs (unpadded large filters on small images: 5x5 on 7x7 computes 49 rows for 9
+// outputs); a cap on that waste (1.7x until round 2) sent such layers to the tap-major
+// gather kernel, which measured 2.9-6.8x slower on every one of them, up to a 49x waste
+// (tools/waste_ab.py: 512x7x7x64 on 7x7, one output per image, 68 vs 302 us) -- so there
+// is no cap by default (tuning waste_pct restores one for A/B).
 static double padded_waste(const ConvGeom& g) {
   const double hq = sw::plane_period(g.h_i, g.h_o, g.k_h, g.s, g.p);
   const double wq = sw::plane_period(g.w_i, g.w_o, g.k_w, g.s, g.p);
@@ -1449,7 +1454,7 @@ static double padded_waste(const ConvGeom& g) {
 
 bool shifted_supported(const ConvGeom& g) {
   if (g.s > 2 || g.k_n % 4 != 0 || g.c_i < 16 || g.k_h * g.k_w > 64) return false;
-  if (padded_waste(g) > 1.7) return false;
+  if (tuning().waste_pct > 0 && padded_waste(g) * 100.0 > (double)tuning().waste_pct) return false;
   const int64_t hq = sw::plane_period(g.h_i, g.h_o, g.k_h, g.s, g.p);
   const int64_t wq = sw::plane_period(g.w_i, g.w_o, g.k_w, g.s, g.p);
   const int64_t dmax = (g.k_h - 1) / g.s + hq * ((g.k_w - 1) / g.s);

@@ -280,7 +280,15 @@ VARIANT_CASES = [
     (dict(k_n=256, k_h=3, k_w=3, c_i=96, h_i=28, w_i=28, b=1, s=2, p=1), "tcgen05-shifted"),
     # 5x5 p=2: the shared-padding plane (14 rows per column instead of 16) keeps it shifted
     (dict(k_n=128, k_h=5, k_w=5, c_i=32, h_i=12, w_i=12, b=2, s=1, p=2), "tcgen05-shifted"),
-    (dict(k_n=64, k_h=7, k_w=7, c_i=32, h_i=6, w_i=6, b=3, s=1, p=3), "tcgen05-gather"),
+    # padded plane 9x9 rows for 6x6 outputs (2.25x): shifted since the waste cap went
+    # (tools/waste_ab.py); with the old 1.7x cap restored it exercises the gather kernel
+    (dict(k_n=64, k_h=7, k_w=7, c_i=32, h_i=6, w_i=6, b=3, s=1, p=3), "tcgen05-shifted"),
+    (dict(k_n=64, k_h=7, k_w=7, c_i=32, h_i=6, w_i=6, b=3, s=1, p=3), "tcgen05-gather", dict(waste_pct=170)),
+    # far more padded rows than outputs: 5x5 on 7x7 unpadded (49 rows for 9 outputs), a
+    # filter as large as the image (one output per image, 25x)
+    (dict(k_n=128, k_h=5, k_w=5, c_i=48, h_i=7, w_i=7, b=9, s=1, p=0), "tcgen05-shifted"),
+    (dict(k_n=64, k_h=5, k_w=5, c_i=32, h_i=5, w_i=5, b=40, s=1, p=0), "tcgen05-shifted"),
+    (dict(k_n=64, k_h=4, k_w=6, c_i=64, h_i=9, w_i=8, b=17, s=2, p=0), "tcgen05-shifted"),
     # wide image: window halo (2 + 2*151 rows) beyond 256 rows (VGG 224x224 layers)
     (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=150, w_i=150, b=1, s=1, p=1), "tcgen05-shifted"),
     # pad > k-1 and asymmetric periods: wrapped reads land in shared zero rows
@@ -330,10 +338,12 @@ def test_tma_fed_1x1_bitwise_equal_to_staged(cp):
 @pytest.mark.parametrize("case", range(len(VARIANT_CASES)))
 @pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
 def test_kernel_variants(orc, case, prec):
-    cp, path = VARIANT_CASES[case]
+    cp, path = VARIANT_CASES[case][:2]
+    tune = VARIANT_CASES[case][2] if len(VARIANT_CASES[case]) > 2 else {}
     F, I = rand_inputs(cp, 100 + case)
     ref = orc.conv_gemm(F, I, cp)
-    O = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo="fused", precision=prec))
+    with cg.tuning(**tune):
+        O = to_host(cg.conv(to_dev(F), to_dev(I), cp, algo="fused", precision=prec))
     if prec == "tf32":
         assert cg.last_path() == path, (cp, cg.last_path())
     else:  # 3xTF32 needs twice the staging; wide polyphase windows fall back to the gather kernel

@@ -18,7 +18,11 @@ from test_fuzz_gpu import draw_big  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--precision", default="tf32")
 ap.add_argument("--n", type=int, default=32)
+ap.add_argument("--tune", default="{}", help="JSON of cgb_set_tuning knobs")
 a = ap.parse_args()
+import json  # noqa: E402
+for k, v in json.loads(a.tune).items():
+    cg.set_tuning(k, v)
 pk = bench.peaks()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 rows = []
