@@ -169,7 +169,7 @@ uint64_t cgb_scratch_cached_bytes(void);
 
 /* ---- dispatch policy (no reference equivalent: the reference's BlockingParams are
  * CPU cache blocking, validated and otherwise ignored here) ----
- * Keys: "sk" (stream-K: 0 never, 1 auto, 2 always), "tail" (tail tiles: 0/1/2), "pair"
+ * Keys: "sk" (stream-K: 0 never, 1 auto, 2 always, 3 auto also for 1x1 layers), "tail" (tail tiles: 0/1/2), "pair"
  * (CTA pairs: 0 never, 1 by policy, 2 also for the low-channel w-im2col layers), "cfg" (force a kernel candidate, -1 auto), "mt", "bn" (force
  * tile sizes, 0 auto), "tma_a", "tma_deep" (1x1-layer variants), "pstore", "pdl",
  * "verbose", "smem_pad_kb", "tps", "splitk", "k2_flo" (explicit 3xTF32: filter lo tile split in

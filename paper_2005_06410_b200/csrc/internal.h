@@ -18,7 +18,7 @@ namespace cgb {
 // (-DCGB_PROFILING, tools/) also take the CGB_* environment variables, read at every
 // launch, plus the correctness-breaking CGB_DEBUG_SW stage switches.
 struct Tuning {
-  int sk = 1;            // stream-K split of the last rounds: 0 never, 1 by fill, 2 whenever it fits
+  int sk = 1;            // stream-K split of the last rounds: 0 never, 1 by fill (3x3-like layers), 2 whenever it fits, 3 by fill incl. 1x1
   int tail = 1;          // tail tiles: 0 never, 1 by cost, 2 whenever they fit
   int pair = 1;          // CTA pairs (cta_group::2): 0 never, 1 by policy, 2 also for the w-im2col layers
   int cfg = -1;          // force one shifted-window candidate (index into kCands)

@@ -66,7 +66,10 @@ def main():
     ap.add_argument("--precisions", default="tf32,3xtf32")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--tune", default="{}", help="JSON of cgb_set_tuning knobs")
     a = ap.parse_args()
+    for k, v in json.loads(a.tune).items():
+        cg.set_tuning(k, v)
     pk = bench.peaks()
     P = pk["tf32_tflops"] * 1e12
     BW = pk["hbm_gbs"] * 1e9

@@ -20,7 +20,11 @@ ap.add_argument("--precision", default="tf32")
 ap.add_argument("--min-time", type=float, default=0.05)
 ap.add_argument("--check", action="store_true")
 ap.add_argument("--out", default=".")
+ap.add_argument("--tune", default="{}", help="JSON of cgb_set_tuning knobs")
 a = ap.parse_args()
+import json  # noqa: E402
+for k, v in json.loads(a.tune).items():
+    cg.set_tuning(k, v)
 for name in a.models.split(","):
     m = models.MODELS[name]()
     rs = cg.run_inference(m, a.batch, algo=a.algo, min_time=a.min_time, check=a.check, precision=a.precision)
