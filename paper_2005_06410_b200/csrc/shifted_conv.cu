@@ -1304,8 +1304,9 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   // 14x14). The fixup itself handles any number of pieces per tile (sk_mode 2 forces it).
   // 1x1 layers (one tap) never gain: a split tile's second piece re-walks output rows the
   // layer is already bound by (14x14 1024->256 b=256: 74.7 us split, 64.6 us as two whole-tile
-  // rounds; 256x1x1x64 on 27x56: 58 vs 48 us), so only sk_mode 2 splits them.
-  const bool sk_ok = !a.tail_mt && (sk_mode == 2 ? (int64_t)tiles * a.CC >= 2 * gmax : tiles >= gmax && (a.taps > 1 || sk_mode == 3));
+  // rounds; 256x1x1x64 on 27x56: 58 vs 48 us), so in TF32 mode only sk_mode 2 or 3 splits them
+  // (3xTF32 1x1 layers are MMA-bound and keep the split: C3 3xTF32 650 us with, 725 us without).
+  const bool sk_ok = !a.tail_mt && (sk_mode == 2 ? (int64_t)tiles * a.CC >= 2 * gmax : tiles >= gmax && (a.taps > 1 || SPLIT || sk_mode == 3));
   if (!a.splitk && sk_mode != 0 && a.CC >= 2 && sk_ok && (fill < kSkFill || sk_mode == 2)) {
     const int dp = std::max(0, tiles / gmax - 1) * gmax;
     const int sk_tiles = tiles - dp;
@@ -1644,7 +1645,7 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
       const int tiles = (int)((a.Mp + units * mt * 128 - 1) / (units * mt * 128)) * n_tiles;
       const int rounds = (tiles + gmax - 1) / gmax;
       const bool sk = tu.sk != 0 && a.CC >= 2 && tiles >= gmax && (double)tiles / (rounds * gmax) < kSkFill &&
-                      (a.taps > 1 || tu.sk >= 2);
+                      (a.taps > 1 || split || tu.sk >= 2);
       const double cost = (sk ? (double)tiles / gmax * 1.03 : (double)rounds) * tt;
       if (cost < best * 0.98) {
         best = cost;
