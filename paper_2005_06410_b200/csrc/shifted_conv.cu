@@ -1646,7 +1646,14 @@ static cudaError_t dispatch(const CUtensorMap& th, const CUtensorMap& tl, const 
       const int rounds = (tiles + gmax - 1) / gmax;
       const bool sk = tu.sk != 0 && a.CC >= 2 && tiles >= gmax && (double)tiles / (rounds * gmax) < kSkFill &&
                       (a.taps > 1 || split || tu.sk >= 2);
-      const double cost = (sk ? (double)tiles / gmax * 1.03 : (double)rounds) * tt;
+      // A split that reaches every tile (fewer than two rounds: no whole-tile round ahead of the
+      // split ones) costs more than its share of a round -- every group pays a fixup and the
+      // filter tile is re-streamed per small tile. With filter tiles <= 128 one round of larger
+      // whole tiles measured 10-15% faster (64x3x3x192 on 56x56 b=16: MT 4 whole 39.9 us vs MT 2
+      // split 46.1; 32x5x5x192 on 28x14 b=128: 77.9 vs 86.9; tools/fuzz_dispatch.py); with
+      // BN = 256 (14x14 256->256) the two measured equal, so the factor applies to BN <= 128 only.
+      const double sk_pen = (sk && tiles < 2 * gmax && bn <= 128) ? tu.sk_pen_pct / 100.0 : 1.0;
+      const double cost = (sk ? (double)tiles / gmax * 1.03 * sk_pen : (double)rounds) * tt;
       if (cost < best * 0.98) {
         best = cost;
         mt_max = mt;
