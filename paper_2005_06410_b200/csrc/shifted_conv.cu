@@ -1188,12 +1188,26 @@ cudaError_t launch_cfg(const CUtensorMap& th, const CUtensorMap& tl, const float
   // keeping at least two groups in the ring.
   {
     const int tap_cycles = MT * a.ksteps * (BN / 2) * (SPLIT ? 3 : 1);
+    // Long layers (>= 8 rounds of tiles per group, filter tiles >= 128, several taps) run in
+    // steady state, where fewer, larger hand-overs win: groups of 3 taps measured 3-9% faster
+    // on VGG's 112x112 and 56x56 layers (112x112 128->128 359 -> 336 us, 56x56 128->256
+    // 171 -> 155, 256->256 312 -> 289; tools/ab_tune.py), while the ResNet-50 3x3 layers
+    // (<= 6 rounds) and VGG's 28x28 / 14x14 layers measured 1-2% slower with them.
+    int thr = 400;
+    {
+      int dev_ = 0, sms_ = 148;
+      cudaGetDevice(&dev_);
+      cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev_);
+      const int64_t rows_ = (int64_t)MT * 128 * (PAIR ? 2 : 1);
+      const int64_t tiles_ = (a.Mp + rows_ - 1) / rows_ * ((a.k_n + BN - 1) / BN);
+      if (!SPLIT && BN >= 128 && a.taps > 1 && !a.wim && tiles_ >= (int64_t)8 * (PAIR ? sms_ / 2 : sms_)) thr = 1100;
+    }
     int g = 1;
     if (tu.tps > 0) {
       g = tu.tps;
     } else {
-      while (g * tap_cycles < 400 && B_STAGES % (g + 1) == 0 && B_STAGES / (g + 1) >= 2) ++g;
-      if (g * tap_cycles < 400)  // the next divisor of the ring (e.g. 3 of 6 after 2 failed)
+      while (g * tap_cycles < thr && B_STAGES % (g + 1) == 0 && B_STAGES / (g + 1) >= 2) ++g;
+      if (g * tap_cycles < thr)  // the next divisor of the ring (e.g. 3 of 6 after 2 failed)
         for (int h = g + 1; h <= B_STAGES / 2; ++h)
           if (B_STAGES % h == 0) { g = h; break; }
     }
