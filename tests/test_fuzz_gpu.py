@@ -135,3 +135,54 @@ def test_random_geometry_large(orc, seed):
         assert e1 <= TOL[prec], (cp, prec, path, e1)
         O2 = cg.conv(F, I, cp, algo="fused", precision=prec)
         assert torch.equal(O, O2), (cp, prec, path)
+
+
+# ---------------------------------------------------------------- high-waste shifted windows
+N_WASTE = 48
+
+
+def draw_waste(seed):
+    """Inside the shifted-window domain (stride <= 2, <= 64 taps, c_i >= 16, k_n % 4 == 0) with
+    far more padded-plane rows than outputs: filters almost as large as the image, little or
+    no padding, 1-4 outputs per dimension (the geometries the old 1.7x waste cap kept away
+    from this kernel)."""
+    rng = np.random.default_rng(9500 + seed)
+    while True:
+        k_h = int(rng.integers(2, 9))
+        k_w = int(rng.integers(1, 9))
+        if k_h * k_w > 64:
+            continue
+        s = int(rng.choice([1, 2]))
+        p = int(rng.choice([0, 0, 1]))
+        o_h, o_w = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+        h_i = (o_h - 1) * s + k_h - 2 * p + int(rng.integers(0, s))
+        w_i = (o_w - 1) * s + k_w - 2 * p + int(rng.integers(0, s))
+        if h_i < 1 or w_i < 1:
+            continue
+        c_i = int(rng.choice([16, 24, 32, 40, 64, 96, 160]))
+        k_n = int(rng.choice([4, 32, 64, 100, 128, 256, 320]))
+        b = int(rng.choice([1, 3, 8, 20, 64, 150]))
+        cp = dict(k_n=k_n, k_h=k_h, k_w=k_w, c_i=c_i, h_i=h_i, w_i=w_i, b=b, s=s, p=p)
+        ho, wo = output_dims_py(cp)
+        if ho < 1 or wo < 1:
+            continue
+        if 2.0 * k_n * ho * wo * b * k_h * k_w * c_i <= 6e8:
+            return cp
+
+
+@pytest.mark.parametrize("seed", range(N_WASTE))
+def test_high_waste_geometry(orc, seed):
+    cp = draw_waste(seed)
+    F, I = rand_inputs(cp, 9600 + seed)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    dF, dI = to_dev(F), to_dev(I)
+    for prec in ("tf32", "auto"):
+        O = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+        path = cg.last_path()
+        err = per_output_error(O, ref, scale)
+        assert err <= TOL[prec], (cp, prec, path, err)
+    assert path in ("tcgen05-shifted", "tcgen05-gather"), (cp, path)
+    with cg.tuning(waste_pct=170):  # the capped dispatch (gather kernel) agrees within the same bar
+        O2 = to_host(cg.conv(dF, dI, cp, algo="fused", precision="auto"))
+    assert per_output_error(O2, ref, scale) <= TOL["auto"], (cp, cg.last_path())
