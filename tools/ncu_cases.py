@@ -5,6 +5,7 @@
   fc6       VGG fc6 (4096 x 25088) at b=64 through cgb_gemm (TF32)
   stem      the 7x7/s2 stem at b=256 (w-im2col mode of the shifted-window kernel)
   pw56      1x1 56^2 64->256 at b=256 (TMA-fed A)
+  vgg56     VGG 56^2 256->256 at b=64 (the shifted-window kernel's best BASELINE layer, 860 TFLOP/s)
   direct    conv_direct (bit-exact reference order) on a small layer
   gather    AlexNet conv1 (11x11 stride 4, 3->64, 224^2) at b=64: outside the shifted-window
             domain (stride > 2), the tap-major gather kernel or the reference-order implicit GEMM
@@ -51,6 +52,9 @@ for _ in range(2):
         cg.gemm(A, B, precision="tf32")
     elif case == "stem":
         cp, F, I = layer("stem_7x7_s2_224")
+        cg.conv(F, I, cp, precision="tf32")
+    elif case == "vgg56":
+        cp, F, I = layer("vgg_56_256_256a")
         cg.conv(F, I, cp, precision="tf32")
     elif case == "pw56":
         cp, F, I = layer("pw_56_64_256")
