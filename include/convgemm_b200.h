@@ -175,7 +175,8 @@ uint64_t cgb_scratch_cached_bytes(void);
  * "verbose", "smem_pad_kb", "tps", "splitk", "k2_flo" (explicit 3xTF32: filter lo tile split in
  * the kernel: -1 never, 0 by size, 1 always), "b_res" (filters resident in the ring when they fit), "urot" (rotate the window unit ->
  * staging warp assignment per chunk), "sk_pen_pct" (M-tile cost model: cost factor in percent of a stream-K split that reaches every tile,
- * filter tiles <= 128; default 130), "waste_pct" (cap on the shifted window's padded-plane rows per
+ * filter tiles <= 128; default 130), "strip_h" (h-strips of that many output rows for wide stride-1 images:
+ * 0 by rule, -1 off), "waste_pct" (cap on the shifted window's padded-plane rows per
  * output row in percent; 0 = none, the default), "host_chunk_kb", "host_no_bounce", "host_copy_threads",
  * "debug" (profiling builds only). Every setting gives a correct result; unknown keys
  * return CGB_INVALID_ARGUMENT. The library reads no environment variables. */

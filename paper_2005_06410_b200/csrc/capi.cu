@@ -57,7 +57,7 @@ static std::mutex g_tune_mu;
 static Tuning g_tune;
 
 #define CGB_TUNING_KEYS(X)                                                                                   \
-  X(sk) X(tail) X(pair) X(cfg) X(mt) X(bn) X(tma_a) X(tma_deep) X(pstore) X(pdl) X(verbose) X(smem_pad_kb) X(tps) X(splitk) X(k2_flo) X(b_res) X(urot) X(waste_pct) X(sk_pen_pct) \
+  X(sk) X(tail) X(pair) X(cfg) X(mt) X(bn) X(tma_a) X(tma_deep) X(pstore) X(pdl) X(verbose) X(smem_pad_kb) X(tps) X(splitk) X(k2_flo) X(b_res) X(urot) X(waste_pct) X(sk_pen_pct) X(strip_h) \
   X(host_chunk_kb) X(host_no_bounce) X(host_copy_threads) X(debug)
 
 Tuning tuning() {

@@ -36,6 +36,7 @@ struct Tuning {
   int urot = 1;          // shifted-window: rotate the window unit -> staging warp assignment per chunk
   int sk_pen_pct = 130;  // M-tile cost model: cost factor (percent) of a stream-K split that reaches every tile
                          // (fewer than two rounds) for filter tiles <= 128; 100 = the round-2 model
+  int strip_h = 0;       // shifted window: h-strips of this many output rows for wide stride-1 images (0 = by rule, -1 = off)
   int waste_pct = 0;     // shifted-window domain: cap on padded-plane rows per real output row, in percent (0 = none)
   int k2_flo = 0;        // explicit 3xTF32: filter lo tile split in the kernel: -1 never, 0 by size, 1 always
   int64_t host_chunk_kb = 8192;  // host path: chunk size of the H2D || conv || D2H pipeline

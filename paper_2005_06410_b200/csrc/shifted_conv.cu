@@ -104,6 +104,11 @@ struct Args {
   // n / (Hq*Wq) and n / Hq as a multiply-shift (n < 2^31): the producers' per-row
   // padded-plane decomposition without integer-division sequences
   uint32_t fd_hwq_m, fd_hwq_p, fd_hq_m, fd_hq_p;
+  // h-strips (wide stride-1 images): each image is cut into `strips` virtual images of strip_h
+  // output rows with the unshared period Hq = strip_h + k_h - 1, so a tile's halo is two strip
+  // columns instead of two image columns. strips = 1: off (strip_h = h_o).
+  int32_t strips, strip_h;
+  uint32_t fd_st_m, fd_st_p;
   unsigned long long* stats;  // per-CTA cycle counters when dbg & 64 (profiling only)
   int32_t dbg;        // profiling switches (CGB_DEBUG_SW): 1 = producers skip loads, 2 = skip MMAs,
                       //   4 = skip epilogue stores, 8 = skip filter TMA
@@ -318,7 +323,12 @@ CGB_DEV void store_units(const Args& a, float* __restrict__ O, uint32_t trow0, i
       const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
       const int32_t rem = Q - bb * hw_q;
       const int32_t wq = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wq * a.Hq;
-      if (hq < a.h_o && wq < a.w_o) P = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
+      if (a.strips > 1) {
+        const int32_t bi = fast_div(bb, a.fd_st_m, a.fd_st_p), h0 = (bb - bi * a.strips) * a.strip_h;
+        if (hq < a.strip_h && h0 + hq < a.h_o && wq < a.w_o) P = (int64_t)(h0 + hq + a.h_o * (wq + a.w_o * bi));
+      } else if (hq < a.h_o && wq < a.w_o) {
+        P = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
+      }
     }
     const uint32_t trow = trow0 + mt * BN;
     uint32_t r[32];
@@ -442,8 +452,15 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(float* __restrict__ 
     const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
     const int32_t rem = Q - bb * hw_q;
     const int32_t wq = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wq * a.Hq;
-    if (hq >= a.h_o || wq >= a.w_o) continue;
-    const int64_t Pix = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
+    int64_t Pix;
+    if (a.strips > 1) {
+      const int32_t bi = fast_div(bb, a.fd_st_m, a.fd_st_p), h0 = (bb - bi * a.strips) * a.strip_h;
+      if (hq >= a.strip_h || h0 + hq >= a.h_o || wq >= a.w_o) continue;
+      Pix = (int64_t)(h0 + hq + a.h_o * (wq + a.w_o * bi));
+    } else {
+      if (hq >= a.h_o || wq >= a.w_o) continue;
+      Pix = (int64_t)(hq + a.h_o * (wq + a.w_o * bb));
+    }
     const int col = (tile / a.m_tiles) * BN + cb * 32 + 4 * j4;
     const float* src = a.sk_ws + ((int64_t)tile * P + rank) * a.splitk * piece + run * 32 + 4 * j4;
     float4 acc = *reinterpret_cast<const float4*>(src);
@@ -577,9 +594,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int32_t bb = fast_div(Q, a.fd_hwq_m, a.fd_hwq_p);
       const int32_t rem = Q - bb * hw_q;
       const int32_t wq = fast_div(rem, a.fd_hq_m, a.fd_hq_p), hq = rem - wq * a.Hq;
-      const int32_t h = a.s * hq + ph_a - a.p, w = a.s * wq + ph_c - a.p;
+      int32_t bi = bb, h0 = 0;
+      if (a.strips > 1) {  // virtual image bb = (image bi, strip): rows continue into the neighbouring strips
+        bi = fast_div(bb, a.fd_st_m, a.fd_st_p);
+        h0 = (bb - bi * a.strips) * a.strip_h;
+      }
+      const int32_t h = a.s * (h0 + hq) + ph_a - a.p, w = a.s * wq + ph_c - a.p;
       ok = (unsigned)h < (unsigned)a.h_i && (unsigned)w < (unsigned)a.w_i;
-      return I + ((int64_t)bb * a.c_i + (int64_t)cc * BK) * a.plane + (w * a.h_i + h);
+      return I + ((int64_t)bi * a.c_i + (int64_t)cc * BK) * a.plane + (w * a.h_i + h);
     };
     auto load_rows = [&](const float* src, bool ok, int cmax, float (&v)[BK]) {
       if (cmax >= BK) {
@@ -1428,10 +1450,30 @@ static Args make_args(const ConvGeom& g) {
   a.NPH = a.nph_h * a.nph_w;
   a.Hq = plane_period(g.h_i, g.h_o, g.k_h, g.s, g.p);
   a.Wq = plane_period(g.w_i, g.w_o, g.k_w, g.s, g.p);
+  a.strips = 1;
+  a.strip_h = a.h_o;
+  {
+    // h-strips for wide stride-1 images: 56 output rows per strip above 112 rows, 28 above 56
+    // (VGG 224x224 64->64 at b=64: 648 -> 431 us; 150x150: 269 -> 222; 5x5 on 131x131: 378 -> 259;
+    // 112x112 64->128 183 -> 175, 128->128 320 -> 314; tools/strip_ab.py). Same UMMAs per output in
+    // the same order: bitwise-equal results. tuning strip_h: 0 = this rule, -1 = off, > 0 forced.
+    const int knob = tuning().strip_h;
+    const int sh = knob > 0 ? knob : (knob < 0 ? 0 : (g.h_o > 112 ? 56 : (g.h_o > 56 ? 28 : 0)));
+    if (sh > 0 && g.s == 1 && g.c_i >= 16 && !(g.k_h == 1 && g.k_w == 1) && g.h_o > 2 * sh) {
+      const int64_t st = (g.h_o + sh - 1) / sh;
+      const int64_t hq = sh + g.k_h - 1;
+      if (hq * a.Wq * g.b * st < (int64_t(1) << 30)) {
+        a.strips = (int32_t)st;
+        a.strip_h = sh;
+        a.Hq = (int32_t)hq;
+      }
+    }
+  }
+  fast_div_magic((uint32_t)a.strips, a.fd_st_m, a.fd_st_p);
   a.dmax = (a.k_h - 1) / a.s + a.Hq * ((a.k_w - 1) / a.s);
   a.CC = (a.c_i + BK - 1) / BK;
   a.taps = a.k_h * a.k_w;
-  a.Mp = (int64_t)a.Hq * a.Wq * g.b;
+  a.Mp = (int64_t)a.Hq * a.Wq * g.b * a.strips;
   a.Mp32 = (int32_t)a.Mp;
   a.plane = g.h_i * g.w_i;
   a.R = 0; a.m_tiles = 0; a.n_tiles = 0;

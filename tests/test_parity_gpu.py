@@ -418,6 +418,45 @@ def test_tail_tiles(orc, case, prec):
         assert np.array_equal(a, b)
 
 
+STRIP_CASES = [
+    # (cp, forced strip height or 0 = the rule): strips that do not divide h_o, pad 0 / 2, 5x5 taps,
+    # non-square images, a batch that leaves the last virtual image ragged
+    (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=150, w_i=150, b=2, s=1, p=1), 0),
+    (dict(k_n=64, k_h=3, k_w=3, c_i=64, h_i=224, w_i=40, b=3, s=1, p=1), 0),
+    (dict(k_n=128, k_h=3, k_w=3, c_i=32, h_i=112, w_i=112, b=2, s=1, p=1), 0),
+    (dict(k_n=64, k_h=5, k_w=5, c_i=32, h_i=131, w_i=37, b=3, s=1, p=2), 0),
+    (dict(k_n=96, k_h=3, k_w=2, c_i=48, h_i=201, w_i=23, b=2, s=1, p=0), 0),
+    (dict(k_n=64, k_h=3, k_w=3, c_i=32, h_i=61, w_i=30, b=5, s=1, p=1), 13),
+    (dict(k_n=256, k_h=3, k_w=3, c_i=64, h_i=70, w_i=20, b=7, s=1, p=2), 17),
+    (dict(k_n=64, k_h=7, k_w=3, c_i=16, h_i=90, w_i=33, b=2, s=1, p=3), 20),
+]
+
+
+@pytest.mark.parametrize("case", range(len(STRIP_CASES)))
+@pytest.mark.parametrize("prec", ("tf32", "3xtf32"))
+def test_h_strips(orc, case, prec):
+    """Wide stride-1 images cut into h-strips (virtual images with halo rows from the
+    neighbouring strips): against the oracle, and bitwise equal to the unstripped launch when
+    neither splits tiles (same UMMAs per output in the same order)."""
+    cp, sh = STRIP_CASES[case]
+    F, I = rand_inputs(cp, 1300 + case)
+    ref = orc.conv_gemm(F, I, cp)
+    scale = orc.output_scale(F, I, cp)
+    dF, dI = to_dev(F), to_dev(I)
+    with cg.tuning(strip_h=sh, sk=0, splitk=-1):
+        a = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+        path = cg.last_path()
+    assert per_output_error(a, ref, scale) <= TOL[prec], (cp, sh, path)
+    with cg.tuning(strip_h=-1, sk=0, splitk=-1):
+        b = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    assert per_output_error(b, ref, scale) <= TOL[prec]
+    if path == "tcgen05-shifted" and cg.last_path() == "tcgen05-shifted":
+        assert np.array_equal(a, b), (cp, sh)
+    with cg.tuning(strip_h=sh):  # default stream-K / split-K on top of the strips
+        c = to_host(cg.conv(dF, dI, cp, algo="fused", precision=prec))
+    assert per_output_error(c, ref, scale) <= TOL[prec], (cp, sh)
+
+
 def _offset_tensor4(a, shift):
     """CUDA leftmost-fastest tensor holding a, starting `shift` floats into its buffer
     (a user pointer that is only 4-byte aligned)."""
